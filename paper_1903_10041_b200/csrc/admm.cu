@@ -1,0 +1,1072 @@
+// admm.cu -- libadmm_b200.so: host runtime behind include/admm.h plus the
+// non-hot kernels (validation, initialisation, objective, state transfer)
+// and the quartic microbench kernel.  Hot path: admm_kernels.cuh.
+//
+// Execution model:
+//   * one CUDA graph per context: a conditional WHILE node whose body is
+//     check_every sweep launches; the last CTA of each sweep sets the
+//     condition (not done and iteration limit not reached), so a whole solve
+//     runs with zero host round trips;
+//   * multi-GPU (world > 1): the body is check_every x [sweep ->
+//     ncclAllGather(per-rank aggregates, 32 doubles) -> finalize_kernel],
+//     driven by a host loop that polls the done flag once per body.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "admm.h"
+#include "admm_kernels.cuh"
+
+using namespace admm_dev;
+
+namespace {
+
+constexpr int HIST_CAP = 8192;
+constexpr int MAX_WORLD = 64;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+    size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
+        row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, total;
+};
+
+int pick_bs(long long n) {
+    long long need = (n + CPT - 1) / CPT;
+    long long bs = ((need + 31) / 32) * 32;
+    return (int)std::max(32LL, std::min(512LL, bs));
+}
+
+Layout make_layout(int m, long long n, long long q, int sms) {
+    Layout L{};
+    const long long n_pad = align_up((size_t)n, 4);
+    const int bs = pick_bs(n);
+    const long long tile = (long long)bs * CPT;
+    const long long T = (n + tile - 1) / tile;
+    const size_t E = (size_t)m * q * n_pad * 8, Cc = (size_t)q * n_pad * 8, R = (size_t)m * q * 8;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o = align_up(o + std::max<size_t>(bytes, 8), 256);
+        return r;
+    };
+    L.a2 = take(E); L.a1 = take(E); L.a0 = take(E); L.b2 = take(E); L.b1 = take(E); L.b0 = take(E);
+    L.lo = take((size_t)m * n_pad * 8); L.hi = take((size_t)m * n_pad * 8);
+    L.y = take(Cc); L.c = take((size_t)m * 8); L.sb0 = take(R);
+    L.x = take(E); L.v = take(Cc);
+    L.lam = take(R); L.zeta = take(R); L.h = take(R); L.p = take(R); L.nu = take(R);
+    L.cta_part = take((size_t)32 * sms * XB * 8);
+    L.row_part = take(T > 1 ? (size_t)m * q * T * 3 * 8 : 8);
+    L.obj_rows = take(R);
+    L.xsend = take(XB * 8); L.xall = take((size_t)MAX_WORLD * XB * 8);
+    L.hist = take((size_t)HIST_CAP * HCOLS * 8);
+    L.row_cnt = take((size_t)q * 4); L.glob_cnt = take(4);
+    L.ctrl = take(2 * sizeof(Ctrl)); L.iter = take(8); L.prm = take(sizeof(DParams));
+    L.vflag = take(8);
+    L.total = o;
+    return L;
+}
+
+// lo/hi of row rix = i*q + j at step k
+__device__ __forceinline__ double lo_of(const KArgs& a, long long rix, long long k) {
+    return a.lo[(rix / a.q) * a.n_pad + k];
+}
+__device__ __forceinline__ double hi_of(const KArgs& a, long long rix, long long k) {
+    return a.hi[(rix / a.q) * a.n_pad + k];
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void validate_kernel(int m, long long q, long long n, long long n_pad,
+                                const double* a2, const double* a1, const double* a0,
+                                const double* b2, const double* b1, const double* b0,
+                                const double* lo, const double* hi, const double* y,
+                                const double* c, unsigned long long* flag) {
+    // code = kind << 56 | linear index; the smallest code is reported
+    const long long NE = (long long)m * q * n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NE; t += stride) {
+        const long long k = t % n, ij = t / n;
+        const long long e = ij * n_pad + k;
+        unsigned long long code = ~0ull;
+        if (!(isfinite(a2[e]) && isfinite(a1[e]) && isfinite(a0[e]) && isfinite(b2[e]) &&
+              isfinite(b1[e]) && isfinite(b0[e])))
+            code = (1ull << 56) | (unsigned long long)t;
+        else if (a2[e] < 0.0) code = (2ull << 56) | (unsigned long long)t;
+        else if (b2[e] < 0.0) code = (3ull << 56) | (unsigned long long)t;
+        if (code != ~0ull) atomicMin(flag, code);
+    }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)m * n;
+         t += stride) {
+        const long long i = t / n, k = t % n;
+        const double l = lo[i * n_pad + k], h = hi[i * n_pad + k];
+        if (!(l <= h) || isnan(l) || isnan(h)) atomicMin(flag, (4ull << 56) | (unsigned long long)t);
+    }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < q * n; t += stride) {
+        const long long j = t / n, k = t % n;
+        if (!isfinite(y[j * n_pad + k])) atomicMin(flag, (5ull << 56) | (unsigned long long)t);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < m && isnan(c[threadIdx.x]))
+        atomicMin(flag, (6ull << 56) | (unsigned long long)threadIdx.x);
+}
+
+// init (reading G19): x = clamp(midpoint) or clamp(0); v = s = max(0, sum_i x - y)
+__global__ void init_cells_kernel(KArgs a) {
+    const long long N = a.q * (long long)a.n_pad;
+    const long long qn = a.q * (long long)a.n_pad;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long j = t / a.n_pad, k = t % a.n_pad;
+        if (k >= a.n) {
+            a.v[t] = 0.0;
+            for (int i = 0; i < a.m; ++i) a.x[i * qn + t] = 0.0;
+            continue;
+        }
+        double sx = 0.0;
+        for (int i = 0; i < a.m; ++i) {
+            const double l = a.lo[i * a.n_pad + k], h = a.hi[i * a.n_pad + k];
+            const double mid = (isfinite(l) && isfinite(h)) ? 0.5 * (l + h) : 0.0;
+            const double xv = clampd(mid, l, h);
+            a.x[i * qn + t] = xv;
+            sx += xv;
+        }
+        a.v[t] = fmax(0.0, sx - a.y[j * a.n_pad + k]);
+    }
+    (void)0;
+}
+
+// block-wide fixed-order sum (blockDim.x == 256)
+__device__ double block_sum_256(double v, double* sh) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < 8 ? sh[threadIdx.x] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;  // valid in threads < 32
+}
+
+// per row (i,j): sb0 = sum_k b0; h = min(c, sum_k g(x)); lam = zeta = p = nu = 0
+__global__ void __launch_bounds__(256) init_rows_kernel(KArgs a) {
+    __shared__ double sh[8];
+    const long long rix = blockIdx.x;  // i * q + j
+    const int i = (int)(rix / a.q);
+    const double* b2 = a.b2 + rix * a.n_pad;
+    const double* b1 = a.b1 + rix * a.n_pad;
+    const double* b0 = a.b0 + rix * a.n_pad;
+    const double* x = a.x + rix * a.n_pad;
+    double sg = 0.0, s0 = 0.0;
+    for (long long k = threadIdx.x; k < a.n; k += 256) {
+        const double xv = x[k];
+        sg += b2[k] * xv * xv + b1[k] * xv + b0[k];
+        s0 += b0[k];
+    }
+    sg = block_sum_256(sg, sh);
+    s0 = block_sum_256(s0, sh);
+    if (threadIdx.x == 0) {
+        ((double*)a.sb0)[rix] = s0;
+        a.h[rix] = fmin(a.c[i], sg);
+        a.lam[rix] = 0.0;
+        a.zeta[rix] = 0.0;
+        a.p[rix] = 0.0;
+        a.nu[rix] = 0.0;
+    }
+}
+
+// consensus partial sums sum_j x_1^{(i,j)} - nu (fixed order) -> xsend
+__global__ void cons_partial_kernel(KArgs a, int with_nu) {
+    if (threadIdx.x >= 32) return;
+    for (int i = 0; i < a.m; ++i) {
+        double s = 0.0;
+        for (long long j = threadIdx.x; j < a.q; j += 32) {
+            const long long rix = (long long)i * a.q + j;
+            s += a.x[rix * a.n_pad] - (with_nu ? a.nu[rix] : 0.0);
+        }
+        s = warp_sum(s);
+        if (threadIdx.x == 0) a.xsend[i] = s;
+    }
+}
+
+__global__ void init_ctrl_kernel(KArgs a, const double* agg, int world, double r0, double r1,
+                                 double r2, double r3) {
+    if (threadIdx.x != 0) return;
+    Ctrl& c = a.ctrl[0];
+    const double rr[4] = {r0, r1, r2, r3};
+    for (int l = 0; l < 4; ++l) {
+        c.rho[l] = rr[l];
+        c.f[l] = 1.0;
+    }
+    for (int i = 0; i < MAXM; ++i) {
+        double s = 0.0;
+        if (i < a.m)
+            for (int r = 0; r < world; ++r) s += agg[r * XB + i];
+        c.x1[i] = i < a.m ? s / (double)a.q_total : 0.0;
+    }
+    c.r = NAN;
+    c.sigma = NAN;
+    c.nu_pending = 0;
+    c.done = 0;
+    c.status = 0;
+    c.checks = 0;
+    c.err = 0;
+    a.ctrl[1] = c;
+    *a.iter = 0;
+    *a.glob_cnt = 0;
+}
+
+// objective rows: sum_k f(x) per (i,j), fixed order
+__global__ void __launch_bounds__(256) obj_rows_kernel(KArgs a, double* out) {
+    __shared__ double sh[8];
+    const long long rix = blockIdx.x;
+    const double* a2 = a.a2 + rix * a.n_pad;
+    const double* a1 = a.a1 + rix * a.n_pad;
+    const double* a0 = a.a0 + rix * a.n_pad;
+    const double* x = a.x + rix * a.n_pad;
+    double s = 0.0;
+    for (long long k = threadIdx.x; k < a.n; k += 256) {
+        const double xv = x[k];
+        s += a2[k] * xv * xv + a1[k] * xv + a0[k];
+    }
+    s = block_sum_256(s, sh);
+    if (threadIdx.x == 0) out[rix] = s;
+}
+
+__global__ void obj_sum_kernel(long long R, const double* rows, double* out) {
+    if (threadIdx.x >= 32) return;
+    double s = 0.0;
+    for (long long r = threadIdx.x; r < R; r += 32) s += rows[r];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+// effective (materialised) state -> dense caller layout
+__global__ void materialize_kernel(KArgs a, double* x, double* z, double* lam, double* s,
+                                   double* mu, double* h, double* p, double* nu, double* x1) {
+    const long long it = *a.iter;
+    const Ctrl& cin = a.ctrl[it & 1];
+    const long long n = a.n, q = a.q;
+    const long long NE = (long long)a.m * q * n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (long long t = t0; t < NE; t += stride) {
+        const long long k = t % n, rix = t / n;
+        const long long e = rix * a.n_pad + k;
+        const double xv = a.x[e];
+        if (x) x[t] = xv;
+        if (z) z[t] = a.b2[e] * xv * xv + a.b1[e] * xv + a.b0[e] + a.zeta[rix];
+        if (lam) lam[t] = a.lam[rix] * cin.f[0];
+    }
+    for (long long t = t0; t < q * n; t += stride) {
+        const long long k = t % n, j = t / n;
+        const double vv = a.v[j * a.n_pad + k];
+        if (s) s[t] = fmax(vv, 0.0);
+        if (mu) mu[t] = vv < 0.0 ? -vv * cin.f[2] : 0.0;
+    }
+    for (long long t = t0; t < (long long)a.m * q; t += stride) {
+        const int i = (int)(t / q);
+        if (h) h[t] = a.h[t];
+        if (p) p[t] = a.p[t] * cin.f[1];
+        if (nu) {
+            double v = a.nu[t];
+            if (cin.nu_pending) v = v + cin.x1[i] - a.x[t * a.n_pad];
+            nu[t] = v * cin.f[3];
+        }
+    }
+    if (x1 && t0 < a.m) x1[t0] = cin.x1[t0];
+}
+
+// warm start: literal arrays -> reduced representation (identities I1, I2)
+__global__ void compress_kernel(KArgs a, const double* x, const double* z, const double* lam,
+                                const double* s, const double* mu, const double* h,
+                                const double* p, const double* nu, unsigned long long* flag) {
+    const long long n = a.n, q = a.q;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long NE = (long long)a.m * q * n;
+    for (long long t = t0; t < NE; t += stride) {
+        const long long k = t % n, rix = t / n;
+        const long long e = rix * a.n_pad + k;
+        a.x[e] = x[t];
+        const double l0 = lam[rix * n];
+        const double g0 = a.b2[rix * a.n_pad] * x[rix * n] * x[rix * n] +
+                          a.b1[rix * a.n_pad] * x[rix * n] + a.b0[rix * a.n_pad];
+        const double ze0 = z[rix * n] - g0;
+        const double gk = a.b2[e] * x[t] * x[t] + a.b1[e] * x[t] + a.b0[e];
+        const double zek = z[t] - gk;
+        if (fabs(lam[t] - l0) > 1e-12 * (1.0 + fabs(l0)))
+            atomicMin(flag, (1ull << 56) | (unsigned long long)t);
+        if (fabs(zek - ze0) > 1e-12 * (1.0 + fabs(z[t]) + fabs(gk)))
+            atomicMin(flag, (2ull << 56) | (unsigned long long)t);
+        const double l = lo_of(a, rix, k), hh = hi_of(a, rix, k);
+        if (!(x[t] >= l && x[t] <= hh)) atomicMin(flag, (4ull << 56) | (unsigned long long)t);
+        if (k == 0) {
+            a.lam[rix] = l0;
+            a.zeta[rix] = ze0;
+        }
+    }
+    for (long long t = t0; t < q * n; t += stride) {
+        const long long k = t % n, j = t / n;
+        const double sv = s[t], mv = mu[t];
+        if (sv < 0.0 || mv < 0.0 || fmin(sv, mv) > 1e-12 * (1.0 + fmax(sv, mv)))
+            atomicMin(flag, (3ull << 56) | (unsigned long long)t);
+        a.v[j * a.n_pad + k] = sv - mv;
+    }
+    for (long long t = t0; t < (long long)a.m * q; t += stride) {
+        a.h[t] = h[t];
+        a.p[t] = p[t];
+        a.nu[t] = nu[t];
+    }
+}
+
+__global__ void set_ctrl_kernel(KArgs a, const double* x1) {
+    if (threadIdx.x != 0) return;
+    const long long it = *a.iter;
+    Ctrl& c = a.ctrl[it & 1];
+    for (int l = 0; l < 4; ++l) c.f[l] = 1.0;
+    for (int i = 0; i < a.m; ++i) c.x1[i] = x1[i];
+    c.nu_pending = 0;
+    c.done = 0;
+}
+
+__global__ void clear_done_kernel(KArgs a) {
+    if (threadIdx.x != 0) return;
+    const long long it = *a.iter;
+    a.ctrl[it & 1].done = 0;
+}
+
+// ---------------------------------------------------------- microbench
+template <int MODE>
+__global__ void __launch_bounds__(256) quartic_batch_vec_kernel(const double* A, const double* B,
+                                                                const double* C, const double* D,
+                                                                const double* lo, const double* hi,
+                                                                double* x, long long N2) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N2; t += stride) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(A) + t);
+        const double2 b = __ldcs(reinterpret_cast<const double2*>(B) + t);
+        const double2 c = __ldcs(reinterpret_cast<const double2*>(C) + t);
+        const double2 d = __ldcs(reinterpret_cast<const double2*>(D) + t);
+        double2 l = make_double2(-INFINITY, -INFINITY), h = make_double2(INFINITY, INFINITY);
+        if (lo) l = __ldcs(reinterpret_cast<const double2*>(lo) + t);
+        if (hi) h = __ldcs(reinterpret_cast<const double2*>(hi) + t);
+        double2 r;
+        r.x = quartic_boxmin<MODE>(a.x, b.x, c.x, d.x, l.x, h.x);
+        r.y = quartic_boxmin<MODE>(a.y, b.y, c.y, d.y, l.y, h.y);
+        __stcs(reinterpret_cast<double2*>(x) + t, r);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) quartic_batch_kernel(const double* A, const double* B,
+                                                            const double* C, const double* D,
+                                                            const double* lo, const double* hi,
+                                                            double* x, long long N) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += stride) {
+        const double l = lo ? lo[t] : -INFINITY, h = hi ? hi[t] : INFINITY;
+        x[t] = quartic_boxmin<MODE>(A[t], B[t], C[t], D[t], l, h);
+    }
+}
+
+}  // namespace
+
+
+// ======================================================================
+// host runtime
+// ======================================================================
+struct admm_ctx {
+    int m = 0;
+    long long n = 0, n_pad = 0, q = 0, q_total = 0, j0 = 0;
+    int device = 0, sms = 148;
+    cudaStream_t stream = nullptr;
+    int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    bool owns_ws = false;
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    Layout L{};
+    KArgs ka{};
+    unsigned long long* vflag = nullptr;
+    double* obj_rows = nullptr;
+    admm_params params{};
+    bool has_problem = false;
+    int bs = 32, T = 1, tile = 64, G = 1;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    int graph_mode = -1;  // box mode the graph was built for
+    std::string err;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    double t_call_ms = 0.0, t_sweep_ms = 0.0;
+    long long iter_host = 0;
+    Ctrl* h_ctrl = nullptr;       // pinned
+    long long* h_iter = nullptr;  // pinned
+    unsigned long long cond = 0;  // cudaGraphConditionalHandle
+};
+
+namespace {
+
+admm_status fail(admm_ctx* c, admm_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CKC(call)                                                                       \
+    do {                                                                                \
+        cudaError_t _e = (call);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(ctx, ADMM_ERR_CUDA,                                             \
+                        std::string(#call) + ": " + cudaGetErrorString(_e));            \
+    } while (0)
+
+#define CKN(call)                                                                       \
+    do {                                                                                \
+        ncclResult_t _r = (call);                                                       \
+        if (_r != ncclSuccess)                                                          \
+            return fail(ctx, ADMM_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+int grid_for(long long work, int bs, int sms) {
+    long long g = (work + bs - 1) / bs;
+    return (int)std::max(1LL, std::min(g, (long long)sms * 8));
+}
+
+void upload_params(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
+    DParams d{};
+    d.tau = ctx->params.tau;
+    d.hi_ratio = ctx->params.hi_ratio;
+    d.lo_ratio = ctx->params.lo_ratio;
+    d.r_bar = ctx->params.r_bar;
+    d.sigma_bar = ctx->params.sigma_bar;
+    d.iter_limit = iter_limit;
+    d.check_every = ctx->params.check_every;
+    d.adapt = ctx->params.adapt_rho;
+    d.rescale = ctx->params.rescale_duals;
+    d.box_mode = ctx->params.box_mode;
+    d.stop_on_conv = stop_on_conv;
+    cudaMemcpyAsync(ctx->ws + ctx->L.prm, &d, sizeof(d), cudaMemcpyHostToDevice, ctx->stream);
+}
+
+typedef void (*sweep_fn)(KArgs);
+
+sweep_fn pick_sweep(int m, int mode) {
+#define S(MM)                                                                                  \
+    if (m == MM) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT> : sweep_kernel<MM, BOX_PROJECT>;
+    S(1) S(2) S(3) S(4)
+#undef S
+    return nullptr;
+}
+
+// body of one while-loop pass: check_every iterations
+admm_status record_body(admm_ctx* ctx, sweep_fn fn) {
+    const int K = std::max(1, ctx->params.check_every);
+    for (int r = 0; r < K; ++r) {
+        fn<<<ctx->G, ctx->bs, 0, ctx->stream>>>(ctx->ka);
+        CKC(cudaGetLastError());
+        if (ctx->world > 1) {
+            CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, ctx->stream));
+            finalize_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ka);
+            CKC(cudaGetLastError());
+        }
+    }
+    return ADMM_OK;
+}
+
+__global__ void set_cond_kernel(KArgs a, cudaGraphConditionalHandle h) {
+    const long long it = *(volatile long long*)a.iter;
+    const Ctrl& c = a.ctrl[it & 1];
+    const bool go = !c.done && it < a.prm->iter_limit;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+admm_status build_graph(admm_ctx* ctx) {
+    if (ctx->gexec && ctx->graph_mode == ctx->params.box_mode) return ADMM_OK;
+    if (ctx->gexec) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+    }
+    if (ctx->graph) {
+        cudaGraphDestroy(ctx->graph);
+        ctx->graph = nullptr;
+    }
+    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode);
+    if (!fn) return fail(ctx, ADMM_ERR_INVALID, "m must be in 1..4");
+    int occ = 0;
+    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, 0));
+    occ = std::max(1, std::min(occ, 32));
+    const long long items = ctx->q * ctx->T;
+    ctx->G = (int)std::max(1LL, std::min(items, (long long)occ * ctx->sms));
+    ctx->ka.G = ctx->G;
+    if (ctx->world == 1) {
+        CKC(cudaGraphCreate(&ctx->graph, 0));
+        cudaGraphConditionalHandle h;
+        CKC(cudaGraphConditionalHandleCreate(&h, ctx->graph, 1, cudaGraphCondAssignDefault));
+        ctx->cond = h;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CKC(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CKC(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal));
+        admm_status st = record_body(ctx, fn);
+        set_cond_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka, h);
+        cudaGraph_t out = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(ctx->stream, &out);
+        if (st != ADMM_OK) return st;
+        CKC(ce);
+    } else {
+        CKC(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        admm_status st = record_body(ctx, fn);
+        cudaError_t ce = cudaStreamEndCapture(ctx->stream, &ctx->graph);
+        if (st != ADMM_OK) return st;
+        CKC(ce);
+    }
+    CKC(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
+    ctx->graph_mode = ctx->params.box_mode;
+    return ADMM_OK;
+}
+
+admm_status read_ctrl(admm_ctx* ctx) {
+    CKC(cudaMemcpyAsync(ctx->h_iter, ctx->ka.iter, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    ctx->iter_host = *ctx->h_iter;
+    CKC(cudaMemcpyAsync(ctx->h_ctrl, ctx->ka.ctrl + (ctx->iter_host & 1), sizeof(Ctrl),
+                        cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    return ADMM_OK;
+}
+
+// run until done or iter_limit, through the graph
+admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
+    if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "set_problem must be called first");
+    admm_status st = build_graph(ctx);
+    if (st != ADMM_OK) return st;
+    upload_params(ctx, iter_limit, stop_on_conv);
+    clear_done_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka);
+    const long long start = ctx->iter_host;
+    CKC(cudaEventRecord(ctx->e0, ctx->stream));
+    if (ctx->world == 1) {
+        CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    } else {
+        const int K = std::max(1, ctx->params.check_every);
+        while (true) {
+            CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
+            st = read_ctrl(ctx);
+            if (st != ADMM_OK) return st;
+            if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
+            (void)K;
+        }
+    }
+    CKC(cudaEventRecord(ctx->e1, ctx->stream));
+    st = read_ctrl(ctx);
+    if (st != ADMM_OK) return st;
+    float ms = 0.f;
+    CKC(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1));
+    ctx->t_call_ms = ms;
+    const long long did = ctx->iter_host - start;
+    ctx->t_sweep_ms = did > 0 ? ms / (double)did : 0.0;
+    if (ctx->h_ctrl->err) return fail(ctx, ADMM_ERR_NUMERICAL, "NaN/Inf in residuals");
+    return ADMM_OK;
+}
+
+void fill_info(admm_ctx* ctx, admm_info* info) {
+    if (!info) return;
+    info->iterations = ctx->iter_host;
+    info->r = ctx->h_ctrl->r;
+    info->sigma = ctx->h_ctrl->sigma;
+    for (int l = 0; l < 4; ++l) info->rho[l] = ctx->h_ctrl->rho[l];
+    info->status = ctx->h_ctrl->status ? ADMM_OK : ADMM_NOT_CONVERGED;
+    info->checks = ctx->h_ctrl->checks;
+}
+
+admm_status compute_objective(admm_ctx* ctx, double* out) {
+    const long long R = (long long)ctx->m * ctx->q;
+    obj_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(ctx->ka, ctx->obj_rows);
+    obj_sum_kernel<<<1, 32, 0, ctx->stream>>>(R, ctx->obj_rows, ctx->ka.xsend);
+    CKC(cudaGetLastError());
+    double tot = 0.0;
+    if (ctx->world > 1) {
+        CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, ctx->stream));
+        std::vector<double> all((size_t)ctx->world * XB);
+        CKC(cudaMemcpyAsync(all.data(), ctx->ka.xall, all.size() * 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+        CKC(cudaStreamSynchronize(ctx->stream));
+        for (int r = 0; r < ctx->world; ++r) tot += all[(size_t)r * XB];
+    } else {
+        CKC(cudaMemcpyAsync(&tot, ctx->ka.xsend, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CKC(cudaStreamSynchronize(ctx->stream));
+    }
+    *out = tot / (double)ctx->q_total;
+    return ADMM_OK;
+}
+
+// copy a dense [rows][n] block (host or device) into a padded [rows][n_pad] array
+admm_status put_rows(admm_ctx* ctx, double* dst, const double* src, long long rows) {
+    if (rows == 0) return ADMM_OK;
+    CKC(cudaMemcpy2DAsync(dst, ctx->n_pad * 8, src, ctx->n * 8, ctx->n * 8, rows, cudaMemcpyDefault,
+                          ctx->stream));
+    return ADMM_OK;
+}
+
+const char* kind_msg(int kind) {
+    switch (kind) {
+        case 1: return "non-finite coefficient";
+        case 2: return "nonconvex cost (a2 < 0)";
+        case 3: return "nonconvex loss (b2 < 0)";
+        case 4: return "inverted or NaN bounds";
+        case 5: return "non-finite demand y";
+        case 6: return "NaN capacity c";
+    }
+    return "invalid";
+}
+
+}  // namespace
+
+extern "C" {
+
+void admm_default_params(admm_params* out) {
+    if (!out) return;
+    // PAPER.md:317-324, :353
+    out->rho[0] = 1e-4;
+    out->rho[1] = 2e-6;
+    out->rho[2] = 5e-6;
+    out->rho[3] = 5e-6;
+    out->tau = 1.1;
+    out->hi_ratio = 1.2;
+    out->lo_ratio = 0.8;
+    out->r_bar = 1e-6;
+    out->sigma_bar = 1e-2;
+    out->check_every = 10;
+    out->adapt_rho = 1;
+    out->rescale_duals = 1;
+    out->box_mode = ADMM_BOX_PROJECT;
+}
+
+size_t admm_workspace_bytes(int32_t m, int64_t n, int64_t q_local, int32_t device) {
+    if (m <= 0 || n <= 0 || q_local <= 0) return 0;
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        cudaGetLastError();
+        sms = 148;
+    }
+    return make_layout(m, n, q_local, sms).total;
+}
+
+admm_status admm_nccl_unique_id(unsigned char out[128]) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return ADMM_ERR_NCCL;
+    static_assert(sizeof(id.internal) == 128, "nccl id size");
+    memcpy(out, id.internal, 128);
+    return ADMM_OK;
+}
+
+admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, const admm_dist* dist,
+                        int32_t device, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+    if (!out) return ADMM_ERR_INVALID;
+    *out = nullptr;
+    if (m < 1 || m > 4 || n < 1 || q_total < 1) return ADMM_ERR_INVALID;
+    admm_ctx* ctx = new admm_ctx();
+    ctx->m = m;
+    ctx->n = n;
+    ctx->n_pad = (long long)align_up((size_t)n, 4);
+    ctx->q_total = q_total;
+    ctx->q = q_total;
+    ctx->device = device;
+    if (dist && dist->world > 1) {
+        if (dist->rank < 0 || dist->rank >= dist->world || dist->world > MAX_WORLD ||
+            dist->j_begin < 0 || dist->j_end <= dist->j_begin || dist->j_end > q_total) {
+            delete ctx;
+            return ADMM_ERR_INVALID;
+        }
+        ctx->world = dist->world;
+        ctx->rank = dist->rank;
+        ctx->j0 = dist->j_begin;
+        ctx->q = dist->j_end - dist->j_begin;
+    }
+    admm_status st = ADMM_OK;
+    auto bail = [&](admm_status s) {
+        *out = ctx;  // keep ctx so the caller can read admm_last_error, then destroy it
+        return s;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(ctx, ADMM_ERR_CUDA, "cudaSetDevice"));
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->L = make_layout(m, n, ctx->q, ctx->sms);
+    if (workspace) {
+        if (workspace_bytes < ctx->L.total)
+            return bail(fail(ctx, ADMM_ERR_INVALID, "workspace too small"));
+        if (((uintptr_t)workspace) % 256 != 0)
+            return bail(fail(ctx, ADMM_ERR_INVALID, "workspace must be 256-byte aligned"));
+        ctx->ws = (char*)workspace;
+    } else {
+        if (cudaMalloc(&ctx->ws, ctx->L.total) != cudaSuccess)
+            return bail(fail(ctx, ADMM_ERR_CUDA, "cudaMalloc workspace"));
+        ctx->owns_ws = true;
+    }
+    ctx->ws_bytes = ctx->L.total;
+    if (cudaMemsetAsync(ctx->ws, 0, ctx->L.total, ctx->stream) != cudaSuccess)
+        return bail(fail(ctx, ADMM_ERR_CUDA, "memset workspace"));
+    if (cudaMallocHost(&ctx->h_ctrl, sizeof(Ctrl)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_iter, 8) != cudaSuccess)
+        return bail(fail(ctx, ADMM_ERR_CUDA, "cudaMallocHost"));
+    memset(ctx->h_ctrl, 0, sizeof(Ctrl));
+    cudaEventCreate(&ctx->e0);
+    cudaEventCreate(&ctx->e1);
+    admm_default_params(&ctx->params);
+    // kernel arguments
+    const Layout& L = ctx->L;
+    KArgs& a = ctx->ka;
+    ctx->bs = pick_bs(n);
+    ctx->tile = ctx->bs * CPT;
+    ctx->T = (int)((n + ctx->tile - 1) / ctx->tile);
+    a.m = m;
+    a.n = (int)n;
+    a.n_pad = (int)ctx->n_pad;
+    a.T = ctx->T;
+    a.tile = ctx->tile;
+    a.G = 1;
+    a.world = ctx->world;
+    a.rank = ctx->rank;
+    a.q = ctx->q;
+    a.q_total = q_total;
+    a.inv_q = 1.0 / (double)q_total;
+    char* w = ctx->ws;
+    a.a2 = (double*)(w + L.a2); a.a1 = (double*)(w + L.a1); a.a0 = (double*)(w + L.a0);
+    a.b2 = (double*)(w + L.b2); a.b1 = (double*)(w + L.b1); a.b0 = (double*)(w + L.b0);
+    a.lo = (double*)(w + L.lo); a.hi = (double*)(w + L.hi); a.y = (double*)(w + L.y);
+    a.c = (double*)(w + L.c); a.sb0 = (double*)(w + L.sb0);
+    a.x = (double*)(w + L.x); a.v = (double*)(w + L.v);
+    a.lam = (double*)(w + L.lam); a.zeta = (double*)(w + L.zeta); a.h = (double*)(w + L.h);
+    a.p = (double*)(w + L.p); a.nu = (double*)(w + L.nu);
+    a.cta_part = (double*)(w + L.cta_part); a.row_part = (double*)(w + L.row_part);
+    a.row_cnt = (int*)(w + L.row_cnt); a.glob_cnt = (int*)(w + L.glob_cnt);
+    a.xsend = (double*)(w + L.xsend); a.xall = (double*)(w + L.xall);
+    a.ctrl = (Ctrl*)(w + L.ctrl); a.iter = (long long*)(w + L.iter);
+    a.prm = (const DParams*)(w + L.prm);
+    a.hist = (double*)(w + L.hist); a.hist_cap = HIST_CAP;
+    ctx->vflag = (unsigned long long*)(w + L.vflag);
+    ctx->obj_rows = (double*)(w + L.obj_rows);
+    if (ctx->world > 1) {
+        ncclUniqueId id;
+        memcpy(id.internal, dist->nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        if (r != ncclSuccess)
+            return bail(fail(ctx, ADMM_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+    }
+    *out = ctx;
+    return st;
+}
+
+admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, const double* lo,
+                             const double* hi, const double* y, const double* c,
+                             int32_t on_device) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (!f || !g || !lo || !hi || !y || !c) return fail(ctx, ADMM_ERR_INVALID, "null argument");
+    (void)on_device;  // cudaMemcpyDefault resolves host vs device pointers (UVA)
+    CKC(cudaSetDevice(ctx->device));
+    KArgs& a = ctx->ka;
+    const long long R = (long long)ctx->m * ctx->q;
+    const size_t blk = (size_t)R * ctx->n;
+    double* fd[3] = {(double*)a.a2, (double*)a.a1, (double*)a.a0};
+    double* gd[3] = {(double*)a.b2, (double*)a.b1, (double*)a.b0};
+    admm_status st;
+    for (int t = 0; t < 3; ++t) {
+        if ((st = put_rows(ctx, fd[t], f + t * blk, R)) != ADMM_OK) return st;
+        if ((st = put_rows(ctx, gd[t], g + t * blk, R)) != ADMM_OK) return st;
+    }
+    if ((st = put_rows(ctx, (double*)a.lo, lo, ctx->m)) != ADMM_OK) return st;
+    if ((st = put_rows(ctx, (double*)a.hi, hi, ctx->m)) != ADMM_OK) return st;
+    if ((st = put_rows(ctx, (double*)a.y, y, ctx->q)) != ADMM_OK) return st;
+    CKC(cudaMemcpyAsync((double*)a.c, c, ctx->m * 8, cudaMemcpyDefault, ctx->stream));
+    // validation (Assumption 1, bounds, finiteness)
+    CKC(cudaMemsetAsync(ctx->vflag, 0xff, 8, ctx->stream));
+    validate_kernel<<<grid_for(blk, 256, ctx->sms), 256, 0, ctx->stream>>>(
+        ctx->m, ctx->q, ctx->n, ctx->n_pad, a.a2, a.a1, a.a0, a.b2, a.b1, a.b0, a.lo, a.hi, a.y,
+        a.c, ctx->vflag);
+    CKC(cudaGetLastError());
+    unsigned long long code = 0;
+    CKC(cudaMemcpyAsync(&code, ctx->vflag, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    if (code != ~0ull) {
+        ctx->has_problem = false;
+        const int kind = (int)(code >> 56);
+        const long long t = (long long)(code & ((1ull << 56) - 1));
+        char buf[160];
+        if (kind <= 3) {
+            const long long k = t % ctx->n, j = (t / ctx->n) % ctx->q, i = t / ctx->n / ctx->q;
+            snprintf(buf, sizeof buf, "%s at (i=%lld,j=%lld,k=%lld)", kind_msg(kind), i, j + ctx->j0, k);
+        } else if (kind == 4) {
+            snprintf(buf, sizeof buf, "%s at (i=%lld,k=%lld)", kind_msg(kind), t / ctx->n, t % ctx->n);
+        } else if (kind == 5) {
+            snprintf(buf, sizeof buf, "%s at (j=%lld,k=%lld)", kind_msg(kind), t / ctx->n + ctx->j0, t % ctx->n);
+        } else {
+            snprintf(buf, sizeof buf, "%s at (i=%lld)", kind_msg(kind), t);
+        }
+        return fail(ctx, (kind == 2 || kind == 3) ? ADMM_ERR_NONCONVEX : ADMM_ERR_INVALID, buf);
+    }
+    // initial state (reading G19)
+    init_cells_kernel<<<grid_for(ctx->q * ctx->n_pad, 256, ctx->sms), 256, 0, ctx->stream>>>(a);
+    init_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(a);
+    cons_partial_kernel<<<1, 32, 0, ctx->stream>>>(a, 0);
+    CKC(cudaGetLastError());
+    const double* agg = a.xsend;
+    if (ctx->world > 1) {
+        CKN(ncclAllGather(a.xsend, a.xall, XB, ncclDouble, ctx->comm, ctx->stream));
+        agg = a.xall;
+    }
+    init_ctrl_kernel<<<1, 32, 0, ctx->stream>>>(a, agg, ctx->world, ctx->params.rho[0],
+                                                 ctx->params.rho[1], ctx->params.rho[2],
+                                                 ctx->params.rho[3]);
+    CKC(cudaMemsetAsync(a.row_cnt, 0, (size_t)ctx->q * 4, ctx->stream));
+    CKC(cudaMemsetAsync(a.hist, 0, (size_t)HIST_CAP * HCOLS * 8, ctx->stream));
+    CKC(cudaGetLastError());
+    ctx->has_problem = true;
+    admm_status rs = read_ctrl(ctx);
+    if (rs != ADMM_OK) return rs;
+    ctx->err.clear();
+    return ADMM_OK;
+}
+
+admm_status admm_set_params(admm_ctx* ctx, const admm_params* p) {
+    if (!ctx || !p) return ADMM_ERR_INVALID;
+    for (int l = 0; l < 4; ++l)
+        if (!(p->rho[l] > 0.0)) return fail(ctx, ADMM_ERR_INVALID, "rho must be > 0");
+    if (!(p->tau >= 1.0) || p->check_every < 1 || !(p->r_bar > 0) || !(p->sigma_bar > 0) ||
+        (p->box_mode != 0 && p->box_mode != 1))
+        return fail(ctx, ADMM_ERR_INVALID, "bad parameters");
+    const bool rebuild = p->check_every != ctx->params.check_every;
+    ctx->params = *p;
+    if (rebuild && ctx->gexec) {
+        cudaGraphExecDestroy(ctx->gexec);
+        ctx->gexec = nullptr;
+        ctx->graph_mode = -1;
+    }
+    if (ctx->has_problem) {
+        // rho takes effect on the next iteration: write it into the current control block
+        const long long it = ctx->iter_host;
+        CKC(cudaMemcpyAsync((char*)(ctx->ka.ctrl + (it & 1)) + offsetof(Ctrl, rho), p->rho,
+                            4 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CKC(cudaStreamSynchronize(ctx->stream));
+    }
+    return ADMM_OK;
+}
+
+admm_status admm_get_params(const admm_ctx* ctx, admm_params* out) {
+    if (!ctx || !out) return ADMM_ERR_INVALID;
+    *out = ctx->params;
+    return ADMM_OK;
+}
+
+admm_status admm_iterate(admm_ctx* ctx, int64_t iters) {
+    if (!ctx || iters < 0) return ADMM_ERR_INVALID;
+    if (iters == 0) return ADMM_OK;
+    CKC(cudaSetDevice(ctx->device));
+    return run_loop(ctx, ctx->iter_host + iters, 0);
+}
+
+admm_status admm_solve(admm_ctx* ctx, double r_bar, double sigma_bar, int64_t max_iter,
+                       admm_info* info) {
+    if (!ctx || !(r_bar > 0) || !(sigma_bar > 0) || max_iter < 0) return ADMM_ERR_INVALID;
+    CKC(cudaSetDevice(ctx->device));
+    ctx->params.r_bar = r_bar;
+    ctx->params.sigma_bar = sigma_bar;
+    admm_status st = run_loop(ctx, ctx->iter_host + max_iter, 1);
+    if (st != ADMM_OK) return st;
+    fill_info(ctx, info);
+    if (info) {
+        st = compute_objective(ctx, &info->objective);
+        if (st != ADMM_OK) return st;
+    }
+    return ctx->h_ctrl->status ? ADMM_OK : ADMM_NOT_CONVERGED;
+}
+
+admm_status admm_get_solution(admm_ctx* ctx, double* x, double* x1, admm_info* info,
+                              int32_t on_device) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "no problem set");
+    (void)on_device;
+    CKC(cudaSetDevice(ctx->device));
+    if (x)
+        CKC(cudaMemcpy2DAsync(x, ctx->n * 8, ctx->ka.x, ctx->n_pad * 8, ctx->n * 8,
+                              (size_t)ctx->m * ctx->q, cudaMemcpyDefault, ctx->stream));
+    admm_status st = read_ctrl(ctx);
+    if (st != ADMM_OK) return st;
+    if (x1) CKC(cudaMemcpyAsync(x1, ctx->h_ctrl->x1, ctx->m * 8, cudaMemcpyDefault, ctx->stream));
+    if (info) {
+        fill_info(ctx, info);
+        st = compute_objective(ctx, &info->objective);
+        if (st != ADMM_OK) return st;
+    }
+    CKC(cudaStreamSynchronize(ctx->stream));
+    return ADMM_OK;
+}
+
+admm_status admm_get_state(admm_ctx* ctx, double* x, double* z, double* lam, double* s, double* mu,
+                           double* h, double* p, double* nu, double* x1, int32_t on_device) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "no problem set");
+    CKC(cudaSetDevice(ctx->device));
+    const size_t E = (size_t)ctx->m * ctx->q * ctx->n, Cn = (size_t)ctx->q * ctx->n,
+                 R = (size_t)ctx->m * ctx->q;
+    double* outs[9] = {x, z, lam, s, mu, h, p, nu, x1};
+    const size_t sz[9] = {E, E, E, Cn, Cn, R, R, R, (size_t)ctx->m};
+    double* dev[9] = {nullptr};
+    size_t tot = 0;
+    for (int t = 0; t < 9; ++t)
+        if (outs[t] && !on_device) tot += sz[t];
+    double* tmp = nullptr;
+    if (tot) CKC(cudaMallocAsync(&tmp, tot * 8, ctx->stream));
+    size_t o = 0;
+    for (int t = 0; t < 9; ++t) {
+        if (!outs[t]) continue;
+        if (on_device) {
+            dev[t] = outs[t];
+        } else {
+            dev[t] = tmp + o;
+            o += sz[t];
+        }
+    }
+    materialize_kernel<<<grid_for(E, 256, ctx->sms), 256, 0, ctx->stream>>>(
+        ctx->ka, dev[0], dev[1], dev[2], dev[3], dev[4], dev[5], dev[6], dev[7], dev[8]);
+    CKC(cudaGetLastError());
+    if (!on_device)
+        for (int t = 0; t < 9; ++t)
+            if (outs[t])
+                CKC(cudaMemcpyAsync(outs[t], dev[t], sz[t] * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (tmp) CKC(cudaFreeAsync(tmp, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    return ADMM_OK;
+}
+
+admm_status admm_set_state(admm_ctx* ctx, const double* x, const double* z, const double* lam,
+                           const double* s, const double* mu, const double* h, const double* p,
+                           const double* nu, const double* x1, int32_t on_device) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "no problem set");
+    if (!x || !z || !lam || !s || !mu || !h || !p || !nu || !x1)
+        return fail(ctx, ADMM_ERR_INVALID, "null argument");
+    CKC(cudaSetDevice(ctx->device));
+    const size_t E = (size_t)ctx->m * ctx->q * ctx->n, Cn = (size_t)ctx->q * ctx->n,
+                 R = (size_t)ctx->m * ctx->q;
+    const double* ins[9] = {x, z, lam, s, mu, h, p, nu, x1};
+    const size_t sz[9] = {E, E, E, Cn, Cn, R, R, R, (size_t)ctx->m};
+    size_t tot = 0;
+    for (int t = 0; t < 9; ++t) tot += sz[t];
+    double* tmp = nullptr;
+    CKC(cudaMallocAsync(&tmp, tot * 8, ctx->stream));
+    const double* dev[9];
+    size_t o = 0;
+    for (int t = 0; t < 9; ++t) {
+        CKC(cudaMemcpyAsync(tmp + o, ins[t], sz[t] * 8, cudaMemcpyDefault, ctx->stream));
+        dev[t] = tmp + o;
+        o += sz[t];
+    }
+    (void)on_device;
+    CKC(cudaMemsetAsync(ctx->vflag, 0xff, 8, ctx->stream));
+    compress_kernel<<<grid_for(E, 256, ctx->sms), 256, 0, ctx->stream>>>(
+        ctx->ka, dev[0], dev[1], dev[2], dev[3], dev[4], dev[5], dev[6], dev[7], ctx->vflag);
+    set_ctrl_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka, dev[8]);
+    CKC(cudaGetLastError());
+    unsigned long long code = 0;
+    CKC(cudaMemcpyAsync(&code, ctx->vflag, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CKC(cudaFreeAsync(tmp, ctx->stream));
+    CKC(cudaStreamSynchronize(ctx->stream));
+    if (code != ~0ull) {
+        const int kind = (int)(code >> 56);
+        const char* what = kind == 1 ? "lambda varies over k" : kind == 2 ? "z - g(x) varies over k"
+                         : kind == 3 ? "s * mu != 0 or negative" : "x outside its box";
+        return fail(ctx, ADMM_ERR_STATE, std::string("state not representable: ") + what);
+    }
+    return read_ctrl(ctx);
+}
+
+int64_t admm_get_history(admm_ctx* ctx, double* out, int64_t max_rows) {
+    if (!ctx || !out || max_rows <= 0 || !ctx->has_problem) return 0;
+    if (read_ctrl(ctx) != ADMM_OK) return 0;
+    const long long nrec = ctx->h_ctrl->checks;
+    const long long avail = std::min<long long>(nrec, HIST_CAP);
+    const long long take = std::min<long long>(avail, max_rows);
+    std::vector<double> all((size_t)HIST_CAP * HCOLS);
+    if (cudaMemcpy(all.data(), ctx->ka.hist, all.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    for (long long r = 0; r < take; ++r) {
+        const long long idx = (nrec - take + r) % HIST_CAP;
+        memcpy(out + r * HCOLS, all.data() + idx * HCOLS, HCOLS * 8);
+    }
+    return take;
+}
+
+admm_status admm_get_timing(admm_ctx* ctx, double out[2]) {
+    if (!ctx || !out) return ADMM_ERR_INVALID;
+    out[0] = ctx->t_sweep_ms;
+    out[1] = ctx->t_call_ms;
+    return ADMM_OK;
+}
+
+const char* admm_last_error(const admm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void admm_destroy(admm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->owns_ws && ctx->ws) cudaFree(ctx->ws);
+    if (ctx->h_ctrl) cudaFreeHost(ctx->h_ctrl);
+    if (ctx->h_iter) cudaFreeHost(ctx->h_iter);
+    if (ctx->e0) cudaEventDestroy(ctx->e0);
+    if (ctx->e1) cudaEventDestroy(ctx->e1);
+    delete ctx;
+}
+
+admm_status quartic_minimize_batch(const double* A, const double* B, const double* C,
+                                   const double* D, const double* lo, const double* hi, double* x,
+                                   int64_t N, int32_t box_mode, void* cuda_stream) {
+    if (N < 0 || !A || !B || !C || !D || !x || (box_mode != 0 && box_mode != 1))
+        return ADMM_ERR_INVALID;
+    if (N == 0) return ADMM_OK;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto al = [](const void* p) { return p == nullptr || ((uintptr_t)p % 16) == 0; };
+    const bool vec = (N % 2 == 0) && al(A) && al(B) && al(C) && al(D) && al(lo) && al(hi) && al(x);
+    const int bs = 256;
+    if (vec) {
+        const long long N2 = N / 2;
+        const int grid = (int)std::min<long long>((N2 + bs - 1) / bs, (long long)sms * 8);
+        if (box_mode == 1)
+            quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+        else
+            quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+    } else {
+        const int grid = (int)std::min<long long>((N + bs - 1) / bs, (long long)sms * 8);
+        if (box_mode == 1)
+            quartic_batch_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N);
+        else
+            quartic_batch_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N);
+    }
+    return cudaGetLastError() == cudaSuccess ? ADMM_OK : ADMM_ERR_CUDA;
+}
+
+const char* admm_build_info(void) {
+    return "libadmm_b200 (arXiv 1903.10041 ADMM hot path), sm_100a fp64, CUDA " 
+#define STR2(x) #x
+#define STR(x) STR2(x)
+        STR(__CUDACC_VER_MAJOR__) "." STR(__CUDACC_VER_MINOR__);
+}
+
+}  // extern "C"

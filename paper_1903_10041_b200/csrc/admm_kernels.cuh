@@ -1,0 +1,577 @@
+// admm_kernels.cuh -- device code of the per-iteration ADMM hot path
+// (Appendix A, Eq. (6a)-(6i), residuals :464-479, adaptive rho
+// :318-324) for sm_100a, fp64.
+//
+// One kernel launch = one ADMM iteration ("sweep"):
+//   * a persistent grid of G CTAs walks work items (scenario j, horizon tile)
+//     in a fixed round-robin order (static => deterministic);
+//   * each thread owns CPT = 2 consecutive steps k of one scenario (128-bit
+//     double2 loads/stores of every SoA stream) and runs the Gauss-Seidel loop
+//     over sources i in registers: build the (6a) quartic, Algorithm 1, box;
+//   * (6e)/(6f) per cell in-thread (reduced state v = s - mu, identity I2);
+//   * (6b)/(6g)/(6d)/(6i) per row (i,j) from a deterministic block reduction of
+//     sum_k g(x_k) (identity I1: lam constant over k, z = g(x) + zeta);
+//     rows longer than one tile are finalised by the last-arriving tile CTA;
+//   * (6c) consensus partial sums and the residual maxima per CTA; the last
+//     CTA to arrive reduces them in CTA order, computes x1, r, sigma, the
+//     termination test and the rho adaptation, and writes the control block
+//     of the next iteration.  (6h) and the dual rescale are applied lazily by
+//     the next sweep when it loads nu / lam / p / mu.
+// DESIGN.md "Kernels" gives the byte model and the readings.
+#pragma once
+#include <cstdint>
+
+#include "quartic.cuh"
+
+namespace admm_dev {
+
+constexpr int MAXM = 8;
+constexpr int CPT = 2;          // cells (steps k) per thread: one double2
+constexpr int XB = 3 * MAXM + 8; // per-rank aggregate: cons[M], x0max[M], x0min[M], r1..r3, s1..s3
+constexpr int HCOLS = 16;
+
+struct Ctrl {
+    double rho[4];   // rho used by the iteration that reads this block
+    double f[4];     // pending rescale of lam, p, mu, nu (rho_old / rho_new)
+    double x1[MAXM]; // consensus x1 of the previous iteration
+    double r, sigma; // last check
+    int nu_pending;  // apply (6h) of the previous iteration on load
+    int done;        // solve converged or numerical error: kernels no-op
+    int status;      // last check met the thresholds
+    int checks;      // checks done
+    int err;         // NaN / Inf in r or sigma
+    int pad[3];
+};
+
+struct DParams {
+    double tau, hi_ratio, lo_ratio, r_bar, sigma_bar;
+    long long iter_limit;  // sweeps with iter >= iter_limit are no-ops
+    int check_every, adapt, rescale, box_mode, stop_on_conv, pad;
+};
+
+struct KArgs {
+    int m, n, n_pad, T, tile, G, world, rank;
+    long long q, q_total;
+    double inv_q;
+    // problem (padded SoA)
+    const double *a2, *a1, *a0, *b2, *b1, *b0;  // [m][q][n_pad]
+    const double *lo, *hi;                      // [m][n_pad]
+    const double *y;                            // [q][n_pad]
+    const double *c;                            // [m]
+    const double *sb0;                          // [m][q]  sum_k b0
+    // reduced state
+    double *x;                                  // [m][q][n_pad]
+    double *v;                                  // [q][n_pad]   s - mu
+    double *lam, *zeta, *h, *p, *nu;            // [m][q]
+    // scratch
+    double *cta_part;                           // [G][XB]
+    double *row_part;                           // [m][q][T][3]
+    int *row_cnt;                               // [q]
+    int *glob_cnt;                              // [1]
+    double *xsend, *xall;                       // [XB], [world][XB]
+    Ctrl *ctrl;                                 // [2]
+    long long *iter;                            // [1] iterations done
+    const DParams *prm;
+    double *hist;
+    int hist_cap;
+};
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ------------------------------------------------------- global finalisation
+// Consumes the per-rank aggregates (rank order), computes (6c), the residuals
+// r / sigma, the termination test and the rho adaptation, and writes the next
+// control block.  Runs on one thread.
+__device__ void finalize_global(const KArgs& a, const double* agg, int world, long long it,
+                                const Ctrl& cin, Ctrl& cout, bool is_check) {
+    const DParams& P = *a.prm;
+    const int m = a.m;
+    // (6c) PAPER.md:436 with the mean (reading G1): x1 = (1/q) sum_j (x_1 - nu)
+    double x1n[MAXM];
+    for (int i = 0; i < m; ++i) {
+        double s = 0.0;
+        for (int r = 0; r < world; ++r) s += agg[r * XB + i];
+        x1n[i] = s / (double)a.q_total;
+    }
+    for (int l = 0; l < 4; ++l) {
+        cout.rho[l] = cin.rho[l];
+        cout.f[l] = 1.0;
+    }
+    for (int i = 0; i < MAXM; ++i) cout.x1[i] = i < m ? x1n[i] : 0.0;
+    cout.r = cin.r;
+    cout.sigma = cin.sigma;
+    cout.nu_pending = 1;
+    cout.done = cin.done;
+    cout.status = cin.status;
+    cout.checks = cin.checks;
+    cout.err = cin.err;
+    if (is_check) {
+        double t[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int r = 0; r < world; ++r) {
+            const double* g = agg + r * XB;
+            t[0] = fmax(t[0], g[3 * MAXM + 0]);
+            t[1] = fmax(t[1], g[3 * MAXM + 1]);
+            t[2] = fmax(t[2], g[3 * MAXM + 2]);
+            for (int i = 0; i < m; ++i) {
+                // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
+                t[3] = fmax(t[3], fmax(g[MAXM + i] - x1n[i], x1n[i] - g[2 * MAXM + i]));
+            }
+            t[4] = fmax(t[4], g[3 * MAXM + 3]);
+            t[5] = fmax(t[5], g[3 * MAXM + 4]);
+            t[6] = fmax(t[6], g[3 * MAXM + 5]);
+        }
+        const double* rho = cin.rho;
+        const double s1 = rho[0] * t[4], s2 = rho[1] * t[5], s3 = rho[2] * t[6];
+        const double r = fmax(fmax(t[0], t[1]), fmax(t[2], t[3]));
+        const double sg = fmax(s1, fmax(s2, s3));
+        const int conv = (r < P.r_bar) && (sg < P.sigma_bar);
+        double fac = 1.0;
+        if (!conv && P.adapt) {
+            const double thr_hi = P.hi_ratio * P.r_bar / P.sigma_bar;
+            const double thr_lo = P.lo_ratio * P.r_bar / P.sigma_bar;
+            const double ratio = (sg > 0.0) ? r / sg : INFINITY;  // reading G12
+            int dir = 0;
+            if (ratio > thr_hi) dir = 1;
+            else if (ratio < thr_lo) dir = -1;
+            if (dir != 0) {
+                for (int l = 0; l < 4; ++l) {
+                    const double old = rho[l];
+                    const double nw = dir > 0 ? old * P.tau : old / P.tau;
+                    cout.rho[l] = nw;
+                    cout.f[l] = P.rescale ? old / nw : 1.0;
+                }
+                fac = dir > 0 ? P.tau : 1.0 / P.tau;
+            }
+        }
+        cout.r = r;
+        cout.sigma = sg;
+        cout.status = conv;
+        cout.checks = cin.checks + 1;
+        if (!isfinite(r) || !isfinite(sg)) {
+            cout.err = 1;
+            cout.done = 1;
+        }
+        if (conv && P.stop_on_conv) cout.done = 1;
+        if (a.hist && a.hist_cap > 0) {
+            double* h = a.hist + (size_t)(cin.checks % a.hist_cap) * HCOLS;
+            h[0] = (double)(it + 1);
+            h[1] = r;
+            h[2] = sg;
+            for (int l = 0; l < 4; ++l) h[3 + l] = rho[l];
+            for (int l = 0; l < 4; ++l) h[7 + l] = t[l];
+            h[11] = s1;
+            h[12] = s2;
+            h[13] = s3;
+            h[14] = conv;
+            h[15] = fac;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- the sweep
+// Row finalisation for (i, j) (PAPER.md:432-448 via identity I1):
+//   W = sum_k (g(x_k) - lam) = Sg + sum_k b0 - n lam,  t = h + p - W,
+//   lam' = kappa t, zeta' = lam' - lam (z' = g(x') + zeta'), 1'z' = W + n lam',
+//   h' = min(c, 1'z' - p), p' = p + h' - 1'z'.
+// Returns the check terms (r2, r3, s1raw, s2raw).
+__device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, int i, long long j,
+                                             double Sg, double dgmax, double dgmin, double* r2,
+                                             double* r3, double* s1, double* s2) {
+    const long long rix = (long long)i * a.q + j;
+    const double nd = (double)a.n;
+    const double lam_e = __ldcg(a.lam + rix) * cin.f[0];
+    const double p_e = __ldcg(a.p + rix) * cin.f[1];
+    const double h_o = __ldcg(a.h + rix);
+    const double zeta_o = __ldcg(a.zeta + rix);
+    const double* rho = cin.rho;
+    const double W = (Sg + a.sb0[rix]) - nd * lam_e;
+    const double kap = rho[1] / (rho[0] + nd * rho[1]);
+    const double t = (h_o + p_e) - W;
+    const double lam_n = kap * t;
+    const double zeta_n = lam_n - lam_e;
+    const double oneTz = W + nd * lam_n;
+    const double h_n = fmin(a.c[i], oneTz - p_e);
+    const double p_n = (p_e + h_n) - oneTz;
+    __stcg(a.lam + rix, lam_n);
+    __stcg(a.zeta + rix, zeta_n);
+    __stcg(a.h + rix, h_n);
+    __stcg(a.p + rix, p_n);
+    const double dz = zeta_n - zeta_o;
+    *r2 = fabs(zeta_n);
+    *r3 = fabs(h_n - oneTz);
+    *s1 = fmax(dgmax + dz, -(dgmin + dz));
+    *s2 = fabs(h_n - h_o);
+}
+
+template <int M, int MODE>
+__global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
+    const long long it = *(volatile long long*)a.iter;
+    const Ctrl& cin = a.ctrl[it & 1];
+    if (cin.done || it >= a.prm->iter_limit) return;
+    const int ce = a.prm->check_every;
+    const bool is_check = ce > 0 && ((it + 1) % ce) == 0;
+
+    __shared__ double red[16][3 * M + 2];
+    __shared__ double rowres[3 * M];
+    __shared__ double k0x[M], k0nu[M];
+    __shared__ double acc[XB];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    if (tid < XB) {
+        double init = 0.0;
+        if (tid >= MAXM && tid < MAXM + M) init = -INFINITY;      // x0max
+        if (tid >= 2 * MAXM && tid < 2 * MAXM + M) init = INFINITY; // x0min
+        acc[tid] = init;
+    }
+
+    double rho[4], f[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        rho[l] = cin.rho[l];
+        f[l] = cin.f[l];
+    }
+    const double iq = a.inv_q;
+    const long long nitems = a.q * a.T;
+    const long long qn = a.q * (long long)a.n_pad;
+
+    double my_r1 = 0.0, my_s3 = 0.0;  // per-thread check maxima over all its cells
+    // row-level check maxima, held by thread i < M for source i
+    double my_r2 = 0.0, my_r3 = 0.0, my_s1 = 0.0, my_s2 = 0.0;
+
+    for (long long item = blockIdx.x; item < nitems; item += a.G) {
+        const long long j = item / a.T;
+        const int tile = (int)(item - j * a.T);
+        const int k = tile * a.tile + CPT * tid;  // first of this thread's 2 cells
+        const bool inb = k < a.n_pad;             // n_pad % 4 == 0: both cells in bounds
+        const bool v0 = k < a.n, v1 = (k + 1) < a.n;
+
+        double xo[M][2], xn[M][2];
+        double Sg[M], dgx[M], dgn[M];
+        double yv[2] = {0, 0}, vv[2] = {0, 0};
+        if (inb) {
+            const double2 t2 = __ldg(reinterpret_cast<const double2*>(a.y + j * a.n_pad + k));
+            yv[0] = t2.x; yv[1] = t2.y;
+            const double2 u2 = *(reinterpret_cast<const double2*>(a.v + j * a.n_pad + k));
+            vv[0] = u2.x; vv[1] = u2.y;
+        }
+        // coefficient streams, all issued up front
+        double ca2[M][2], ca1[M][2], cb2[M][2], cb1[M][2], clo[M][2], chi[M][2];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            if (inb) {
+                const long long e = (long long)i * qn + j * a.n_pad + k;
+                double2 t;
+                t = *(reinterpret_cast<const double2*>(a.x + e));  xo[i][0] = t.x; xo[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.a2 + e)); ca2[i][0] = t.x; ca2[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.a1 + e)); ca1[i][0] = t.x; ca1[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.b2 + e)); cb2[i][0] = t.x; cb2[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.b1 + e)); cb1[i][0] = t.x; cb1[i][1] = t.y;
+                const long long bk = (long long)i * a.n_pad + k;
+                t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    xo[i][c] = 0; ca2[i][c] = 0; ca1[i][c] = 0; cb2[i][c] = 0; cb1[i][c] = 0;
+                    clo[i][c] = 0; chi[i][c] = 0;
+                }
+            }
+        }
+        // per-row scalars (uniform loads)
+        double lam_e[M], zeta_o[M], nu_e[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const long long rix = (long long)i * a.q + j;
+            lam_e[i] = __ldcg(a.lam + rix) * f[0];
+            zeta_o[i] = __ldcg(a.zeta + rix);
+            nu_e[i] = 0.0;
+        }
+        const bool owns_k0 = (k == 0);
+        if (owns_k0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const long long rix = (long long)i * a.q + j;
+                double nu = __ldcg(a.nu + rix);
+                // lazy (6h) of the previous iteration, then its dual rescale
+                if (cin.nu_pending) nu = nu + cin.x1[i] - xo[i][0];
+                nu_e[i] = nu * f[3];
+                __stcg(a.nu + rix, nu_e[i]);
+            }
+        }
+
+        // ---- (6a) Gauss-Seidel over sources, per cell
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            // s, mu of the previous iteration (identity I2) with mu's pending rescale
+            const double s_e = fmax(vv[c], 0.0);
+            const double mu_e = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
+            const bool kk0 = owns_k0 && c == 0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double others = 0.0;
+#pragma unroll
+                for (int l = 0; l < M; ++l)
+                    if (l != i) others += (l < i) ? xn[l][c] : xo[l][c];
+                const double phi = ((s_e - others) + yv[c]) + mu_e;
+                const double xoi = xo[i][c];
+                const double b2 = cb2[i][c], b1 = cb1[i][c];
+                // e = theta - b0 = g(x_old) + zeta + lam - b0 (z = g(x) + zeta, I1)
+                const double e = fma(fma(b2, xoi, b1), xoi, zeta_o[i] + lam_e[i]);
+                const double A = 0.5 * rho[0] * b2 * b2;
+                const double B = rho[0] * b2 * b1;
+                double C = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i][c], iq, 0.5 * rho[2]));
+                double D = fma(-rho[0] * b1, e, fma(ca1[i][c], iq, -rho[2] * phi));
+                if (kk0) {
+                    C += 0.5 * rho[3];
+                    D += -rho[3] * (cin.x1[i] + nu_e[i]);
+                }
+                xn[i][c] = quartic_boxmin<MODE>(A, B, C, D, clo[i][c], chi[i][c]);
+            }
+        }
+
+        // ---- (6e)/(6f) per cell, row partials of (6b), check terms
+        double vn[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const bool valid = c == 0 ? v0 : v1;
+            double sx = 0.0, dx = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                sx += xn[i][c];
+                dx += xn[i][c] - xo[i][c];
+            }
+            const double mu_e = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
+            const double s_o = fmax(vv[c], 0.0);
+            const double vnew = (sx - yv[c]) - mu_e;
+            const double s_n = fmax(vnew, 0.0);
+            vn[c] = valid ? vnew : 0.0;
+            if (is_check && valid) {
+                my_r1 = fmax(my_r1, fabs((s_n - sx) + yv[c]));
+                my_s3 = fmax(my_s3, fabs((s_n - s_o) - dx));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            Sg[i] = 0.0;
+            dgx[i] = -INFINITY;
+            dgn[i] = INFINITY;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const bool valid = c == 0 ? v0 : v1;
+                if (!valid) xn[i][c] = 0.0;  // padding stays 0
+                if (valid) {
+                    const double b2 = cb2[i][c], b1 = cb1[i][c];
+                    Sg[i] += fma(b2, xn[i][c], b1) * xn[i][c];
+                    const double dg = (xn[i][c] - xo[i][c]) * fma(b2, xn[i][c] + xo[i][c], b1);
+                    dgx[i] = fmax(dgx[i], dg);
+                    dgn[i] = fmin(dgn[i], dg);
+                }
+            }
+        }
+        if (inb) {
+            *(reinterpret_cast<double2*>(a.v + j * a.n_pad + k)) = make_double2(vn[0], vn[1]);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const long long e = (long long)i * qn + j * a.n_pad + k;
+                *(reinterpret_cast<double2*>(a.x + e)) = make_double2(xn[i][0], xn[i][1]);
+            }
+        }
+        if (owns_k0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                k0x[i] = xn[i][0];
+                k0nu[i] = nu_e[i];
+            }
+        }
+
+        // ---- deterministic block reduction of Sg (sum), dg (max/min) per source
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            Sg[i] = warp_sum(Sg[i]);
+            if (is_check) {
+                dgx[i] = warp_max(dgx[i]);
+                dgn[i] = warp_min(dgn[i]);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                red[wid][3 * i] = Sg[i];
+                red[wid][3 * i + 1] = dgx[i];
+                red[wid][3 * i + 2] = dgn[i];
+            }
+        }
+        __syncthreads();
+        if (wid == 0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double s = lane < nw ? red[lane][3 * i] : 0.0;
+                double mx = lane < nw ? red[lane][3 * i + 1] : -INFINITY;
+                double mn = lane < nw ? red[lane][3 * i + 2] : INFINITY;
+                s = warp_sum(s);
+                if (is_check) {
+                    mx = warp_max(mx);
+                    mn = warp_min(mn);
+                }
+                if (lane == 0) {
+                    rowres[3 * i] = s;
+                    rowres[3 * i + 1] = mx;
+                    rowres[3 * i + 2] = mn;
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- row finalisation (6b),(6g),(6d),(6i)
+        if (a.T == 1) {
+            if (tid < M) {
+                double r2, r3, s1, s2;
+                finalize_row(a, cin, tid, j, rowres[3 * tid], rowres[3 * tid + 1],
+                             rowres[3 * tid + 2], &r2, &r3, &s1, &s2);
+                my_r2 = fmax(my_r2, r2);
+                my_r3 = fmax(my_r3, r3);
+                my_s1 = fmax(my_s1, s1);
+                my_s2 = fmax(my_s2, s2);
+            }
+        } else {
+            if (tid < M) {
+                double* rp = a.row_part + (((long long)tid * a.q + j) * a.T + tile) * 3;
+                __stcg(rp, rowres[3 * tid]);
+                __stcg(rp + 1, rowres[3 * tid + 1]);
+                __stcg(rp + 2, rowres[3 * tid + 2]);
+            }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = (atomicAdd(a.row_cnt + j, 1) == a.T - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                if (tid < M) {
+                    const double* rp = a.row_part + ((long long)tid * a.q + j) * a.T * 3;
+                    double Sgs = 0.0, mx = -INFINITY, mn = INFINITY;
+                    for (int t = 0; t < a.T; ++t) {
+                        Sgs += __ldcg(rp + 3 * t);
+                        mx = fmax(mx, __ldcg(rp + 3 * t + 1));
+                        mn = fmin(mn, __ldcg(rp + 3 * t + 2));
+                    }
+                    double r2, r3, s1, s2;
+                    finalize_row(a, cin, tid, j, Sgs, mx, mn, &r2, &r3, &s1, &s2);
+                    my_r2 = fmax(my_r2, r2);
+                    my_r3 = fmax(my_r3, r3);
+                    my_s1 = fmax(my_s1, s1);
+                    my_s2 = fmax(my_s2, s2);
+                }
+                if (tid == 0) a.row_cnt[j] = 0;
+            }
+        }
+        // ---- (6c) consensus contributions of k = 0, in this CTA's item order
+        if (tile == 0 && tid < M) {
+            acc[tid] += k0x[tid] - k0nu[tid];
+            acc[MAXM + tid] = fmax(acc[MAXM + tid], k0x[tid]);
+            acc[2 * MAXM + tid] = fmin(acc[2 * MAXM + tid], k0x[tid]);
+        }
+        __syncthreads();  // red/rowres/k0x reused by the next item
+    }
+
+    // ---- per-CTA partials: block max of r1, s3; row maxima of threads < M
+    if (is_check) {
+        my_r1 = warp_max(my_r1);
+        my_s3 = warp_max(my_s3);
+        if (lane == 0) {
+            red[wid][0] = my_r1;
+            red[wid][1] = my_s3;
+        }
+        if (tid < M) {
+            rowres[tid] = my_r2;
+            rowres[M + tid] = my_r3;
+            rowres[2 * M + tid] = my_s1;
+            k0x[tid] = my_s2;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double r1 = 0.0, s3 = 0.0, r2 = 0.0, r3 = 0.0, s1 = 0.0, s2 = 0.0;
+            for (int w = 0; w < nw; ++w) {
+                r1 = fmax(r1, red[w][0]);
+                s3 = fmax(s3, red[w][1]);
+            }
+            for (int i = 0; i < M; ++i) {
+                r2 = fmax(r2, rowres[i]);
+                r3 = fmax(r3, rowres[M + i]);
+                s1 = fmax(s1, rowres[2 * M + i]);
+                s2 = fmax(s2, k0x[i]);
+            }
+            acc[3 * MAXM + 0] = r1;
+            acc[3 * MAXM + 1] = r2;
+            acc[3 * MAXM + 2] = r3;
+            acc[3 * MAXM + 3] = s1;
+            acc[3 * MAXM + 4] = s2;
+            acc[3 * MAXM + 5] = s3;
+        }
+        __syncthreads();
+    }
+    if (tid < XB) __stcg(a.cta_part + (size_t)blockIdx.x * XB + tid, acc[tid]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.glob_cnt, 1) == a.G - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+
+    // ---- last CTA: reduce CTA partials in CTA order (warp 0, fixed tree)
+    if (wid == 0) {
+        for (int s = 0; s < XB; ++s) {
+            const bool is_sum = s < MAXM;
+            const bool is_min = s >= 2 * MAXM && s < 3 * MAXM;
+            double v = is_sum ? 0.0 : (is_min ? INFINITY : -INFINITY);
+            if (s >= 3 * MAXM) v = 0.0;
+            for (int g = lane; g < a.G; g += 32) {
+                const double t = __ldcg(a.cta_part + (size_t)g * XB + s);
+                v = is_sum ? v + t : (is_min ? fmin(v, t) : fmax(v, t));
+            }
+            v = is_sum ? warp_sum(v) : (is_min ? warp_min(v) : warp_max(v));
+            if (lane == 0) a.xsend[s] = v;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        *a.glob_cnt = 0;
+        if (a.world == 1) {
+            __threadfence();
+            Ctrl& cout = a.ctrl[(it + 1) & 1];
+            finalize_global(a, a.xsend, 1, it, cin, cout, is_check);
+            __threadfence();
+            *(volatile long long*)a.iter = it + 1;
+        }
+    }
+}
+
+// multi-GPU: after ncclAllGather(xsend -> xall) on the stream
+__global__ void finalize_kernel(KArgs a) {
+    const long long it = *(volatile long long*)a.iter;
+    const Ctrl& cin = a.ctrl[it & 1];
+    if (cin.done || it >= a.prm->iter_limit) return;
+    if (threadIdx.x != 0) return;
+    const int ce = a.prm->check_every;
+    const bool is_check = ce > 0 && ((it + 1) % ce) == 0;
+    finalize_global(a, a.xall, a.world, it, cin, a.ctrl[(it + 1) & 1], is_check);
+    __threadfence();
+    *(volatile long long*)a.iter = it + 1;
+}
+
+}  // namespace admm_dev
