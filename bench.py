@@ -1,0 +1,481 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the ADMM hot path (arXiv 1903.10041) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload phev|toy|horizon|sweep|microbench] [--q Q] [--n N]
+
+Default workload = BASELINE.json configs[1]: PHEV robust energy management,
+m=2 (engine, battery), n=1000, q=50 scenarios per GPU, solved to the paper's
+thresholds (r_bar = 1e-6 dE, sigma_bar = 1e-2, checks every 10 iterations,
+adaptive rho).  One step = one solve from the initial
+state (admm_reset + admm_solve): every ADMM iteration runs all §8(a) rows
+(quartic build, Algorithm 1, box, demand and capacity couplings, consensus,
+duals, residuals, rho).  The metric is element-updates/s = m n q_total x
+iterations / s (BASELINE.json "metric"), iterations/s alongside.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): scenarios are sharded (weak
+scaling: q = 50 per GPU), with one all-gather of 32 doubles per iteration
+inside the library.  Timing: W warm-up steps; L2 flushed (512 MiB write)
+before every timed step; each step bracketed by CUDA events on the solver's
+stream; barrier + synchronize around the timed loop; max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="phev",
+                    choices=["phev", "toy", "horizon", "sweep", "microbench"])
+    ap.add_argument("--q", type=int, default=None, help="scenarios per GPU (phev/sweep)")
+    ap.add_argument("--n", type=int, default=None, help="horizon (horizon workload)")
+    ap.add_argument("--family", default="R", help="microbench quartic family (R or C)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workloads
+def workload(args, rank, world):
+    """Returns a dict describing the per-rank problem and the step."""
+    import synth
+    from paper_1903_10041_b200.dist import shard_range
+
+    w = args.workload
+    if w == "microbench":
+        return dict(kind="quartic", N=100_000_000, family=args.family,
+                    name=f"quartic-minimiser microbench: 1e8 random quartics (family "
+                         f"{args.family}), box bounds, fp64 (BASELINE.json configs[4])")
+    if w == "phev":
+        qg = args.q or 50
+        n = 1000
+        q_total = qg * world
+        j0, j1 = shard_range(q_total, rank, world)
+        P = synth.phev_problem(n, j1 - j0, j0=j0)
+        dE = P["c"][1]
+        return dict(kind="solve", P=P, m=2, n=n, q_total=q_total, r_bar=1e-6 * dE, sigma_bar=1e-2,
+                    max_iter=20000,
+                    name=f"PHEV robust energy management m=2 n=1000 q={qg}/GPU, solve to "
+                         f"r<1e-6 dE, sigma<1e-2 (BASELINE.json configs[1])")
+    if w == "toy":
+        P = synth.toy_problem()
+        return dict(kind="iterate", P=P, m=2, n=10, q_total=1, iters=200,
+                    r_bar=1e-6 * P["c"][1], sigma_bar=1e-2,
+                    name="nominal toy n=10 m=2 q=1, 200 fixed iterations (BASELINE.json configs[0])")
+    if w == "horizon":
+        n = args.n or 100_000
+        P = synth.horizon_problem(n)
+        return dict(kind="solve", P=P, m=4, n=n, q_total=1, r_bar=1e-6 * P["c"][2],
+                    sigma_bar=1e-2, max_iter=20000,
+                    name=f"horizon sweep m=4 q=1 n={n}, solve to tol (BASELINE.json configs[2])")
+    if w == "sweep":
+        qg = args.q or 10000
+        q_total = qg * world
+        j0, j1 = shard_range(q_total, rank, world)
+        P = synth.phev_problem(1000, j1 - j0, j0=j0)
+        return dict(kind="iterate", P=P, m=2, n=1000, q_total=q_total, iters=100,
+                    r_bar=1e-6 * P["c"][1], sigma_bar=1e-2,
+                    name=f"scenario sweep n=1000 m=2 q={qg}/GPU, 100 fixed iterations per step "
+                         f"(BASELINE.json configs[3])")
+    raise ValueError(w)
+
+
+def alg_bytes_per_iter(m, n, q):
+    """Algorithmic bytes one sweep must move (SURVEY.md
+    §8(d)): per element a2,a1,b2,b1 + x read/write; per cell y + v read/write;
+    per (i,k) lo,hi; per row lam,zeta,h,p read+write, sum b0, nu read/write."""
+    return 8 * (6 * m * q * n + 3 * q * n + 2 * m * n + 11 * m * q)
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def ncu_traffic(workload_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    summary (profiles/), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(workload_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self, device):
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+        except Exception:
+            return None
+        rows = [r for r in rows if len(r) >= 9 and r[0].strip() == str(device)]
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]),
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1903_10041_b200 as L
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    W = workload(args, rank, world)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    if W["kind"] == "quartic":
+        return run_quartic(args, W, dev, flush)
+
+    P = W["P"]
+    m, n, q_total = W["m"], W["n"], W["q_total"]
+    q_loc = P["q"]
+    dist = None
+    if world > 1:
+        dist = L.make_dist(q_total)
+    s = L.AdmmSolver(m, n, q_total, device=local_rank, dist=dist, r_bar=W["r_bar"],
+                     sigma_bar=W["sigma_bar"])
+    s.set_problem(P)
+
+    def step():
+        s.reset()
+        if W["kind"] == "solve":
+            info = s.solve(W["r_bar"], W["sigma_bar"], W["max_iter"])
+            return info["iterations"], info
+        s.iterate(W["iters"])
+        return W["iters"], None
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    iters, sweep_ms, infos = [], [], []
+    clk = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
+                       if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                       else f"/tmp/clocks_rank{rank}.csv")
+    with clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            it, info = step()
+            ev[k][1].record(stream)
+            iters.append(it)
+            infos.append(info)
+            sweep_ms.append(s.timing()[0])
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_ms, op=torch.distributed.ReduceOp.MAX)
+    T = float(t_ms.item()) / 1e3
+    tot_iters = int(sum(iters))
+    elem = m * n * q_total
+    value = elem * tot_iters / T
+    it_per_s = tot_iters / T
+    # dominant kernel: the fused sweep (one launch per iteration)
+    avg_sweep_ms = float(np.mean(sweep_ms))
+    ab = alg_bytes_per_iter(m, n, q_loc)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    achieved = ab / (avg_sweep_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": "sweep_kernel (one launch = one ADMM iteration)",
+            "achieved": achieved, "peak": hbm if hbm else 6650.0, "unit": "GB/s",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6.65 TB/s",
+            "frac": achieved / (hbm if hbm else 6650.0),
+            "traffic": ncu_traffic(args.workload),
+            "alg_bytes_per_launch": ab, "avg_launch_ms": avg_sweep_ms,
+            "launch_ms_note": "event time of the graph / iterations (includes the 1-in-10 "
+                              "set-condition kernel and inter-kernel gaps: an upper bound)"}
+    res = dict(value=value, it_per_s=it_per_s, T=T, iters=iters, step_ms=step_ms,
+               roof=roof, W=W, clocks=clk.summary(local_rank), infos=infos)
+    # launches per step: reset (4 kernels) + clear_done + sweeps + set_cond per 10 + objective (2)
+    K = max(1, s.params.check_every)
+    per = [4 + 1 + (-(-it // K)) * K + (-(-it // K)) + (2 if W["kind"] == "solve" else 0)
+           for it in iters]
+    res["gpu_launches"] = int(sum(per))
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(args, s, W, dev, flush, world)
+    s.close()
+    return res
+
+
+def run_e2e(args, s, W, dev, flush, world):
+    """Same metric through the public API with pinned HOST buffers: per step
+    set_problem (H2D of every input) -> solve/iterate -> get_solution (D2H)."""
+    import numpy as np
+    import torch
+
+    P = W["P"]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    f = pin(np.stack([P["a2"], P["a1"], P["a0"]]))
+    g = pin(np.stack([P["b2"], P["b1"], P["b0"]]))
+    lo, hi, y, c = pin(P["lo"]), pin(P["hi"]), pin(P["y"]), pin(P["c"])
+    x = torch.empty((W["m"], P["q"], W["n"]), dtype=torch.float64).pin_memory()
+    x1 = torch.empty(W["m"], dtype=torch.float64).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        s.set_problem_packed(f, g, lo, hi, y, c)
+        if W["kind"] == "solve":
+            it = s.solve(W["r_bar"], W["sigma_bar"], W["max_iter"])["iterations"]
+        else:
+            s.iterate(W["iters"])
+            it = W["iters"]
+        s.solution(x, x1)
+        return it
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    tot, its = 0.0, 0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        its += step()
+        b.record(stream)
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    t = torch.tensor([tot], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    T = float(t.item()) / 1e3
+    h2d = sum(int(v.numel() * 8) for v in (f, g, lo, hi, y, c))
+    d2h = int(x.numel() * 8 + x1.numel() * 8)
+    return {"value": W["m"] * W["n"] * W["q_total"] * its / T, "unit": "element-updates/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "iterations_per_s": its / T,
+            "path": "AdmmSolver.set_problem_packed(pinned host) -> solve -> solution(pinned host)"}
+
+
+def run_quartic(args, W, dev, flush):
+    import torch
+
+    import paper_1903_10041_b200 as L
+    import synth
+
+    N = W["N"]
+    A, B, C, D, lo, hi = synth.quartic_family(W["family"], N, device=dev)
+    x = torch.empty_like(A)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        L.quartic_minimize_batch(A, B, C, D, lo, hi, out=x)
+    torch.cuda.synchronize()
+    ms = []
+    with ClockSampler("/tmp/clocks_q.csv") as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            L.quartic_minimize_batch(A, B, C, D, lo, hi, out=x)
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    T = sum(ms) / 1e3
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    avg = T / args.steps
+    achieved = 56 * N / avg / 1e9
+    res = dict(value=N * args.steps / T, T=T, iters=[1] * args.steps, step_ms=ms, W=W,
+               clocks=clk.summary(dev.index), gpu_launches=args.steps,
+               roof={"bound": "hbm", "kernel": "quartic_batch_vec_kernel", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": ncu_traffic("microbench"), "alg_bytes_per_launch": 56 * N,
+                     "avg_launch_ms": avg * 1e3})
+    del A, B, C, D, lo, hi
+    if not args.no_e2e:
+        # e2e: host (pinned) coefficients -> device -> minimise -> host
+        n_e = 20_000_000
+        hs = [t.cpu().pin_memory() for t in synth.quartic_family(W["family"], n_e, device="cpu")]
+        xo = torch.empty(n_e, dtype=torch.float64).pin_memory()
+        tot = 0.0
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ds = [h.to(dev, non_blocking=True) for h in hs]
+            xd = L.quartic_minimize_batch(*ds)
+            xo.copy_(xd, non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        res["e2e"] = {"value": n_e * args.steps / (tot / 1e3), "unit": "quartics/s",
+                      "h2d_bytes_per_step": 48 * n_e, "d2h_bytes_per_step": 8 * n_e,
+                      "sample": f"{n_e:.0e} quartics per step"}
+    return res
+
+
+# ------------------------------------------------------------ oracle (CPU)
+def oracle_rate(args, W, budget_s=12.0, per_step=False):
+    """The CPU oracle as it stands, single thread, on a bounded sample of the
+    same workload: returns (value, sample description, seconds)."""
+    import numpy as np
+
+    import oracle
+
+    if W["kind"] == "quartic":
+        import synth
+
+        Ns = 5_000_000 if not per_step else 2_000_000
+        A, B, C, D, lo, hi = (t.numpy() for t in synth.quartic_family(W["family"], Ns))
+        t0 = time.perf_counter()
+        oracle.quartic_batch(A, B, C, D, lo, hi, 0)
+        dt = time.perf_counter() - t0
+        return Ns / dt, f"{Ns:.0e} quartics of family {W['family']}", dt
+    P = W["P"]
+    prm = oracle.default_params(r_bar=W["r_bar"], sigma_bar=W["sigma_bar"])
+    o = oracle.Oracle(P, prm, q_total=W["q_total"] if W["q_total"] == P["q"] else None)
+    elem = P["m"] * P["n"] * P["q"]
+    # size the sample: ~190 ns per element-update
+    iters = max(1, int(budget_s / (elem * 1.9e-7)))
+    if W["kind"] == "iterate":
+        iters = min(iters, W["iters"])
+    t0 = time.perf_counter()
+    o.run(iters)
+    dt = time.perf_counter() - t0
+    return elem * iters / dt, (f"first {iters} ADMM iterations of the same workload from the "
+                               f"initial state ({elem} element-updates each), 1 thread"), dt
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return main_reference(args, rank, world)
+
+    import torch
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    W = res["W"]
+    unit = "quartics/s" if W["kind"] == "quartic" else "element-updates/s"
+    line = {
+        "metric": ("quartic minimisations/s (Algorithm 1 + box, fp64)" if W["kind"] == "quartic"
+                   else "ADMM element-updates/s (m*n*q x iterations/s; iterations/s alongside)"),
+        "value": res["value"], "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["T"] * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded PHEV-shaped generator, synth/)",
+        "config": {"workload": W["name"], "l2": "flushed (512 MiB write) before each timed step",
+                   "parallelism": f"scenario-sharded dp{world}" if world > 1 else "1 GPU"},
+        "gpu_launches": res["gpu_launches"], "roofline": res["roof"],
+    }
+    if W["kind"] != "quartic":
+        line["config"].update(m=W["m"], n=W["n"], q_total=W["q_total"],
+                              iterations_per_step=res["iters"])
+        line["iterations_per_s"] = res["it_per_s"]
+    if "e2e" in res:
+        line["e2e"] = res["e2e"]
+    if res.get("clocks"):
+        line["clocks"] = res["clocks"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample, dt = oracle_rate(args, W)
+        line["cpu_baseline"] = {"value": v, "unit": unit, "cores": 1, "kind": "oracle",
+                                "sample": sample, "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main_reference(args, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm) timed as it
+    stands on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    if args.workload != "microbench" and args.q is None and world > 1:
+        args.q = 50
+    W = workload(args, 0, 1) if world == 1 else workload(args, 0, 1)
+    unit = "quartics/s" if W["kind"] == "quartic" else "element-updates/s"
+    for _ in range(args.warmup):
+        oracle_rate(args, W, budget_s=2.0, per_step=True)
+    vals, tot = [], 0.0
+    for _ in range(args.steps):
+        v, sample, dt = oracle_rate(args, W, budget_s=4.0, per_step=True)
+        vals.append(v)
+        tot += dt
+    value = sum(vals) / len(vals)
+    line = {"impl": "reference", "metric": ("quartic minimisations/s (Algorithm 1 + box, fp64)"
+                                            if W["kind"] == "quartic" else
+                                            "ADMM element-updates/s (m*n*q x iterations/s; "
+                                            "iterations/s alongside)"),
+            "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded PHEV-shaped generator, synth/)",
+            "config": {"workload": W["name"]},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

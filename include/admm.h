@@ -72,6 +72,13 @@ typedef enum {
     ADMM_BOX_EXACT = 1    /* x <- argmin_box J: block minimiser of L */
 } admm_box_mode;
 
+typedef enum {
+    ADMM_EXEC_AUTO = 0,       /* persistent when the state fits on chip, else streaming */
+    ADMM_EXEC_STREAMING = 1,  /* one fused sweep kernel per iteration, CUDA-graph while loop */
+    ADMM_EXEC_PERSISTENT = 2  /* one cooperative kernel per call, state in shared memory;
+                                 ADMM_ERR_INVALID if the problem does not fit on chip */
+} admm_exec_mode;
+
 /* Scenario sharding across ranks (one process per GPU).  Rank r owns the
    scenarios j in [j_begin, j_end) of q_total.  nccl_id comes from
    admm_nccl_unique_id on rank 0, broadcast by the caller (torch.distributed). */
@@ -83,7 +90,8 @@ typedef struct {
 
 /* Parameters; admm_default_params() fills the paper's values (PAPER.md:317-324,
    :353): rho = (1e-4, 2e-6, 5e-6, 5e-6), tau = 1.1, band 1.2 / 0.8,
-   sigma_bar = 1e-2, check_every = 10, adapt on, dual rescale on, PROJECT. */
+   sigma_bar = 1e-2, check_every = 10, adapt on, dual rescale on, PROJECT,
+   exec_mode AUTO. */
 typedef struct {
     double rho[4];          /* rho1..rho4 used from the next iteration on */
     double tau, hi_ratio, lo_ratio;
@@ -92,6 +100,7 @@ typedef struct {
     int32_t adapt_rho;      /* adapt rho at each check */
     int32_t rescale_duals;  /* scaled duals *= rho_old/rho_new on adaptation (reading G11) */
     int32_t box_mode;       /* admm_box_mode */
+    int32_t exec_mode;      /* admm_exec_mode (execution engine; results agree to rounding) */
 } admm_params;
 
 typedef struct {
@@ -133,6 +142,12 @@ admm_status admm_create(admm_ctx** ctx, int32_t m, int64_t n, int64_t q_total,
    h = min(c, 1'z), p = 0, x1 = mean_j x_1^{(i,j)}, nu = 0, rho = params.rho. */
 admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, const double* lo,
                              const double* hi, const double* y, const double* c, int32_t on_device);
+
+/* Re-initialise the state from the current problem data exactly as
+   admm_set_problem does (reading G19), with rho = params.rho and the
+   iteration counter, checks and history cleared.  No host<->device copies of
+   problem data. */
+admm_status admm_reset(admm_ctx* ctx);
 
 /* Replace the parameters.  rho takes effect on the next iteration. */
 admm_status admm_set_params(admm_ctx* ctx, const admm_params* params);

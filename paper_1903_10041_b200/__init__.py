@@ -26,6 +26,7 @@ from ._lib import (  # noqa: F401
     admm_iterate,
     admm_last_error,
     admm_nccl_unique_id,
+    admm_reset,
     admm_set_params,
     admm_set_problem,
     admm_set_state,

@@ -26,6 +26,7 @@ _lib = C.CDLL(SO_PATH)
 ADMM_OK, ADMM_ERR_INVALID, ADMM_NOT_CONVERGED, ADMM_ERR_NONCONVEX = 0, 1, 2, 3
 ADMM_ERR_NUMERICAL, ADMM_ERR_CUDA, ADMM_ERR_NCCL, ADMM_ERR_STATE = 4, 5, 6, 7
 ADMM_BOX_PROJECT, ADMM_BOX_EXACT = 0, 1
+ADMM_EXEC_AUTO, ADMM_EXEC_STREAMING, ADMM_EXEC_PERSISTENT = 0, 1, 2
 ADMM_HIST_COLS = 16
 STATUS_NAMES = {0: "ADMM_OK", 1: "ADMM_ERR_INVALID", 2: "ADMM_NOT_CONVERGED",
                 3: "ADMM_ERR_NONCONVEX", 4: "ADMM_ERR_NUMERICAL", 5: "ADMM_ERR_CUDA",
@@ -41,7 +42,7 @@ class admm_params(C.Structure):
     _fields_ = [("rho", C.c_double * 4), ("tau", C.c_double), ("hi_ratio", C.c_double),
                 ("lo_ratio", C.c_double), ("r_bar", C.c_double), ("sigma_bar", C.c_double),
                 ("check_every", C.c_int32), ("adapt_rho", C.c_int32),
-                ("rescale_duals", C.c_int32), ("box_mode", C.c_int32)]
+                ("rescale_duals", C.c_int32), ("box_mode", C.c_int32), ("exec_mode", C.c_int32)]
 
 
 class admm_info(C.Structure):
@@ -64,6 +65,7 @@ _sigs = {
     "admm_create": (C.c_int, [C.POINTER(_ctx_p), C.c_int32, C.c_int64, C.c_int64,
                               C.POINTER(admm_dist), C.c_int32, _vp, C.c_size_t, _vp]),
     "admm_set_problem": (C.c_int, [_ctx_p, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int32]),
+    "admm_reset": (C.c_int, [_ctx_p]),
     "admm_set_params": (C.c_int, [_ctx_p, C.POINTER(admm_params)]),
     "admm_get_params": (C.c_int, [_ctx_p, C.POINTER(admm_params)]),
     "admm_iterate": (C.c_int, [_ctx_p, C.c_int64]),
@@ -157,6 +159,10 @@ def admm_set_problem(ctx, f, g, lo, hi, y, c):
     ps = [_ptr(a) for a in (f, g, lo, hi, y, c)]
     on_dev = int(any(p[1] for p in ps))
     return _check(ctx, _lib.admm_set_problem(ctx, *[p[0] for p in ps], on_dev))
+
+
+def admm_reset(ctx):
+    return _check(ctx, _lib.admm_reset(ctx))
 
 
 def admm_set_params(ctx, params: admm_params):

@@ -17,12 +17,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "admm.h"
 #include "admm_kernels.cuh"
+#include "admm_persist.cuh"
 
 using namespace admm_dev;
 
@@ -35,7 +37,8 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
-        row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, total;
+        row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
+        prc, pbar, total;
 };
 
 int pick_bs(long long n) {
@@ -70,6 +73,13 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.row_cnt = take((size_t)q * 4); L.glob_cnt = take(4);
     L.ctrl = take(2 * sizeof(Ctrl)); L.iter = take(8); L.prm = take(sizeof(DParams));
     L.vflag = take(8);
+    // persistent-kernel scratch (used only when q*T <= 32*sms CTAs)
+    const size_t GP = (size_t)32 * sms;
+    L.pg = take(2 * (size_t)m * GP * 3 * 8);
+    L.pc = take(2 * (size_t)m * std::min<size_t>(q, GP) * 2 * 8);
+    L.pr = take(2 * GP * 2 * 8);
+    L.prc = take(2 * (size_t)m * std::min<size_t>(q, GP) * 4 * 8);
+    L.pbar = take(64 * 4);
     L.total = o;
     return L;
 }
@@ -387,7 +397,8 @@ struct admm_ctx {
     int m = 0;
     long long n = 0, n_pad = 0, q = 0, q_total = 0, j0 = 0;
     int device = 0, sms = 148;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // caller's stream: all work is ordered on it
+    cudaStream_t cap_stream = nullptr;  // private stream used only to capture the graph
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     bool owns_ws = false;
@@ -410,6 +421,8 @@ struct admm_ctx {
     Ctrl* h_ctrl = nullptr;       // pinned
     long long* h_iter = nullptr;  // pinned
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
+    bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
+    int last_engine = 0;          // 1 streaming, 2 persistent (last call)
 };
 
 namespace {
@@ -466,14 +479,14 @@ sweep_fn pick_sweep(int m, int mode) {
 }
 
 // body of one while-loop pass: check_every iterations
-admm_status record_body(admm_ctx* ctx, sweep_fn fn) {
+admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
     const int K = std::max(1, ctx->params.check_every);
     for (int r = 0; r < K; ++r) {
-        fn<<<ctx->G, ctx->bs, 0, ctx->stream>>>(ctx->ka);
+        fn<<<ctx->G, ctx->bs, 0, st>>>(ctx->ka);
         CKC(cudaGetLastError());
         if (ctx->world > 1) {
-            CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, ctx->stream));
-            finalize_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ka);
+            CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, st));
+            finalize_kernel<<<1, 32, 0, st>>>(ctx->ka);
             CKC(cudaGetLastError());
         }
     }
@@ -518,18 +531,18 @@ admm_status build_graph(admm_ctx* ctx) {
         cudaGraphNode_t node;
         CKC(cudaGraphAddNode(&node, ctx->graph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        CKC(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+        CKC(cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
-        admm_status st = record_body(ctx, fn);
-        set_cond_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka, h);
+        admm_status st = record_body(ctx, fn, ctx->cap_stream);
+        set_cond_kernel<<<1, 1, 0, ctx->cap_stream>>>(ctx->ka, h);
         cudaGraph_t out = nullptr;
-        cudaError_t ce = cudaStreamEndCapture(ctx->stream, &out);
+        cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &out);
         if (st != ADMM_OK) return st;
         CKC(ce);
     } else {
-        CKC(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        admm_status st = record_body(ctx, fn);
-        cudaError_t ce = cudaStreamEndCapture(ctx->stream, &ctx->graph);
+        CKC(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+        admm_status st = record_body(ctx, fn, ctx->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &ctx->graph);
         if (st != ADMM_OK) return st;
         CKC(ce);
     }
@@ -548,16 +561,116 @@ admm_status read_ctrl(admm_ctx* ctx) {
     return ADMM_OK;
 }
 
+typedef void (*persist_fn)(KArgs, PArgs);
+
+persist_fn pick_persist(int m, int mode) {
+#define S(MM)                                                                                  \
+    if (m == MM) return mode == BOX_EXACT ? persist_kernel<MM, BOX_EXACT> : persist_kernel<MM, BOX_PROJECT>;
+    S(1) S(2) S(3) S(4)
+#undef S
+    return nullptr;
+}
+
+struct PPlan {
+    bool ok = false;
+    int TC = 0, T = 0, G = 0, BS = 0;
+    size_t smem = 0;
+};
+
+// tile the (j, k) plane so that every SM gets about one CTA and each CTA's
+// state fits in shared memory; all CTAs must be co-resident
+PPlan plan_persist(admm_ctx* ctx, persist_fn fn) {
+    PPlan pl;
+    if (ctx->world > 1 || !fn) return pl;
+    const long long n = ctx->n, q = ctx->q;
+    const int sms = ctx->sms;
+    long long T = std::max<long long>((n + 1023) / 1024, q <= sms ? sms / q : 1);
+    T = std::min<long long>(T, (n + 63) / 64);
+    T = std::max<long long>(T, 1);
+    long long TC = 0;
+    size_t smem = 0;
+    for (int guard = 0; guard < 4096; ++guard) {
+        const long long per = (n + T - 1) / T;
+        TC = 64 * ((per + 63) / 64);
+        T = (n + TC - 1) / TC;
+        smem = (size_t)(7 * ctx->m + 2) * TC * 8;
+        if (smem <= 200 * 1024) break;
+        ++T;
+    }
+    const long long G = q * T;
+    if (G > 32LL * sms) return pl;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return pl;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, (int)(TC / 2), smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return pl;
+    }
+    if ((long long)occ * sms < G) return pl;
+    pl.ok = true;
+    pl.TC = (int)TC;
+    pl.T = (int)T;
+    pl.G = (int)G;
+    pl.BS = (int)(TC / 2);
+    pl.smem = smem;
+    return pl;
+}
+
+admm_status launch_persist(admm_ctx* ctx, persist_fn fn, const PPlan& pl) {
+    PArgs pa;
+    pa.TC = pl.TC;
+    pa.T = pl.T;
+    pa.G = pl.G;
+    pa.gpart = (double*)(ctx->ws + ctx->L.pg);
+    pa.cpart = (double*)(ctx->ws + ctx->L.pc);
+    pa.rpart = (double*)(ctx->ws + ctx->L.pr);
+    pa.rowchk = (double*)(ctx->ws + ctx->L.prc);
+    pa.bar = (unsigned*)(ctx->ws + ctx->L.pbar);
+    KArgs ka = ctx->ka;
+    void* args[] = {&ka, &pa};
+    CKC(cudaLaunchCooperativeKernel((const void*)fn, pl.G, pl.BS, args, pl.smem, ctx->stream));
+    return ADMM_OK;
+}
+
 // run until done or iter_limit, through the graph
 admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "set_problem must be called first");
-    admm_status st = build_graph(ctx);
-    if (st != ADMM_OK) return st;
+    admm_status st = ADMM_OK;
+    PPlan pl;
+    persist_fn pfn = nullptr;
+    if (ctx->params.exec_mode != ADMM_EXEC_STREAMING) {
+        pfn = pick_persist(ctx->m, ctx->params.box_mode);
+        pl = plan_persist(ctx, pfn);
+        if (!pl.ok && ctx->params.exec_mode == ADMM_EXEC_PERSISTENT)
+            return fail(ctx, ADMM_ERR_INVALID, "problem does not fit the persistent engine");
+    }
+    if (!pl.ok) {
+        st = build_graph(ctx);
+        if (st != ADMM_OK) return st;
+    }
+    ctx->last_engine = pl.ok ? 2 : 1;
     upload_params(ctx, iter_limit, stop_on_conv);
     clear_done_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka);
     const long long start = ctx->iter_host;
     CKC(cudaEventRecord(ctx->e0, ctx->stream));
-    if (ctx->world == 1) {
+    if (pl.ok) {
+        st = launch_persist(ctx, pfn, pl);
+        if (st != ADMM_OK) return st;
+    } else if (ctx->no_graph) {
+        // profiling mode (ADMM_NO_GRAPH=1): plain launches, host polls per body
+        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode);
+        while (true) {
+            st = record_body(ctx, fn, ctx->stream);
+            if (st != ADMM_OK) return st;
+            st = read_ctrl(ctx);
+            if (st != ADMM_OK) return st;
+            if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
+        }
+    } else if (ctx->world == 1) {
         CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
     } else {
         const int K = std::max(1, ctx->params.check_every);
@@ -632,6 +745,28 @@ const char* kind_msg(int kind) {
     return "invalid";
 }
 
+// initial state from the current problem (reading G19)
+admm_status init_state(admm_ctx* ctx) {
+    KArgs& a = ctx->ka;
+    const long long R = (long long)ctx->m * ctx->q;
+    init_cells_kernel<<<grid_for(ctx->q * ctx->n_pad, 256, ctx->sms), 256, 0, ctx->stream>>>(a);
+    init_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(a);
+    cons_partial_kernel<<<1, 32, 0, ctx->stream>>>(a, 0);
+    CKC(cudaGetLastError());
+    const double* agg = a.xsend;
+    if (ctx->world > 1) {
+        CKN(ncclAllGather(a.xsend, a.xall, XB, ncclDouble, ctx->comm, ctx->stream));
+        agg = a.xall;
+    }
+    init_ctrl_kernel<<<1, 32, 0, ctx->stream>>>(a, agg, ctx->world, ctx->params.rho[0],
+                                                 ctx->params.rho[1], ctx->params.rho[2],
+                                                 ctx->params.rho[3]);
+    CKC(cudaMemsetAsync(a.row_cnt, 0, (size_t)ctx->q * 4, ctx->stream));
+    CKC(cudaMemsetAsync(a.hist, 0, (size_t)HIST_CAP * HCOLS * 8, ctx->stream));
+    CKC(cudaGetLastError());
+    return ADMM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -652,6 +787,7 @@ void admm_default_params(admm_params* out) {
     out->adapt_rho = 1;
     out->rescale_duals = 1;
     out->box_mode = ADMM_BOX_PROJECT;
+    out->exec_mode = ADMM_EXEC_AUTO;
 }
 
 size_t admm_workspace_bytes(int32_t m, int64_t n, int64_t q_local, int32_t device) {
@@ -724,7 +860,13 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     memset(ctx->h_ctrl, 0, sizeof(Ctrl));
     cudaEventCreate(&ctx->e0);
     cudaEventCreate(&ctx->e1);
+    if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(ctx, ADMM_ERR_CUDA, "cudaStreamCreate"));
     admm_default_params(&ctx->params);
+    {
+        const char* ng = getenv("ADMM_NO_GRAPH");
+        ctx->no_graph = ng && ng[0] == '1';
+    }
     // kernel arguments
     const Layout& L = ctx->L;
     KArgs& a = ctx->ka;
@@ -816,22 +958,8 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
         }
         return fail(ctx, (kind == 2 || kind == 3) ? ADMM_ERR_NONCONVEX : ADMM_ERR_INVALID, buf);
     }
-    // initial state (reading G19)
-    init_cells_kernel<<<grid_for(ctx->q * ctx->n_pad, 256, ctx->sms), 256, 0, ctx->stream>>>(a);
-    init_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(a);
-    cons_partial_kernel<<<1, 32, 0, ctx->stream>>>(a, 0);
-    CKC(cudaGetLastError());
-    const double* agg = a.xsend;
-    if (ctx->world > 1) {
-        CKN(ncclAllGather(a.xsend, a.xall, XB, ncclDouble, ctx->comm, ctx->stream));
-        agg = a.xall;
-    }
-    init_ctrl_kernel<<<1, 32, 0, ctx->stream>>>(a, agg, ctx->world, ctx->params.rho[0],
-                                                 ctx->params.rho[1], ctx->params.rho[2],
-                                                 ctx->params.rho[3]);
-    CKC(cudaMemsetAsync(a.row_cnt, 0, (size_t)ctx->q * 4, ctx->stream));
-    CKC(cudaMemsetAsync(a.hist, 0, (size_t)HIST_CAP * HCOLS * 8, ctx->stream));
-    CKC(cudaGetLastError());
+    admm_status is = init_state(ctx);
+    if (is != ADMM_OK) return is;
     ctx->has_problem = true;
     admm_status rs = read_ctrl(ctx);
     if (rs != ADMM_OK) return rs;
@@ -839,12 +967,21 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
     return ADMM_OK;
 }
 
+admm_status admm_reset(admm_ctx* ctx) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "no problem set");
+    CKC(cudaSetDevice(ctx->device));
+    admm_status st = init_state(ctx);
+    if (st != ADMM_OK) return st;
+    return read_ctrl(ctx);
+}
+
 admm_status admm_set_params(admm_ctx* ctx, const admm_params* p) {
     if (!ctx || !p) return ADMM_ERR_INVALID;
     for (int l = 0; l < 4; ++l)
         if (!(p->rho[l] > 0.0)) return fail(ctx, ADMM_ERR_INVALID, "rho must be > 0");
     if (!(p->tau >= 1.0) || p->check_every < 1 || !(p->r_bar > 0) || !(p->sigma_bar > 0) ||
-        (p->box_mode != 0 && p->box_mode != 1))
+        (p->box_mode != 0 && p->box_mode != 1) || p->exec_mode < 0 || p->exec_mode > 2)
         return fail(ctx, ADMM_ERR_INVALID, "bad parameters");
     const bool rebuild = p->check_every != ctx->params.check_every;
     ctx->params = *p;
@@ -1029,6 +1166,7 @@ void admm_destroy(admm_ctx* ctx) {
     if (ctx->h_iter) cudaFreeHost(ctx->h_iter);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
     if (ctx->e1) cudaEventDestroy(ctx->e1);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     delete ctx;
 }
 

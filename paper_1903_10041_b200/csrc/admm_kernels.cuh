@@ -27,7 +27,8 @@ namespace admm_dev {
 
 constexpr int MAXM = 8;
 constexpr int CPT = 2;          // cells (steps k) per thread: one double2
-constexpr int XB = 3 * MAXM + 8; // per-rank aggregate: cons[M], x0max[M], x0min[M], r1..r3, s1..s3
+constexpr int XB = 3 * MAXM + 8; // = 32 per-rank aggregate slots: cons[M], x0max[M], x0min[M], r1..r3, s1..s3
+static_assert(XB == 32, "one warp lane per aggregate slot");
 constexpr int HCOLS = 16;
 
 struct Ctrl {
@@ -93,6 +94,147 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
+// ------------------------------------------------ per-cell / per-row math
+// (6a) for one cell (j,k): Gauss-Seidel over sources i = 0..M-1
+// (PAPER.md:423-429 in the theta/phi form :452-463; reading G2).
+//   phi   = s - sum_{l != i} x^{(l)} + y + mu   (new x for l < i, old for l > i)
+//   e     = theta - b0 = g(x_old) + zeta + lam - b0      (identity I1: z = g(x) + zeta)
+//   A..D  = coefficients of the (6a) quartic
+// zl[i] = zeta + lam_e of row (i,j); x1nu[i] = x1 + nu_e (used when k0).
+template <int M, int MODE>
+__device__ __forceinline__ void gs_cell(const double* ca2, const double* ca1, const double* cb2,
+                                        const double* cb1, const double* clo, const double* chi,
+                                        const double* xo, double* xn, double y, double s_e,
+                                        double mu_e, const double* zl, const double* rho, double iq,
+                                        bool k0, const double* x1nu) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double others = 0.0;
+#pragma unroll
+        for (int l = 0; l < M; ++l)
+            if (l != i) others += (l < i) ? xn[l] : xo[l];
+        const double phi = ((s_e - others) + y) + mu_e;
+        const double xoi = xo[i];
+        const double b2 = cb2[i], b1 = cb1[i];
+        const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
+        const double A = 0.5 * rho[0] * b2 * b2;
+        const double B = rho[0] * b2 * b1;
+        double C = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i], iq, 0.5 * rho[2]));
+        double D = fma(-rho[0] * b1, e, fma(ca1[i], iq, -rho[2] * phi));
+        if (k0) {
+            C += 0.5 * rho[3];
+            D += -rho[3] * x1nu[i];
+        }
+        xn[i] = quartic_boxmin<MODE>(A, B, C, D, clo[i], chi[i]);
+    }
+}
+
+// (6e)/(6f) for one cell with the reduced state v = s - mu (identity I2);
+// returns v_new and updates the check maxima |s - sum x + y| and
+// |(s - s~) - sum_i (x - x~)|.
+template <int M>
+__device__ __forceinline__ double cell_tail(const double* xo, const double* xn, double y,
+                                            double v_old, double f3, bool chk, double& r1,
+                                            double& s3) {
+    double sx = 0.0, dx = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        sx += xn[i];
+        dx += xn[i] - xo[i];
+    }
+    const double mu_e = v_old < 0.0 ? -v_old * f3 : 0.0;
+    const double s_o = fmax(v_old, 0.0);
+    const double vnew = (sx - y) - mu_e;
+    if (chk) {
+        const double s_n = fmax(vnew, 0.0);
+        r1 = fmax(r1, fabs((s_n - sx) + y));
+        s3 = fmax(s3, fabs((s_n - s_o) - dx));
+    }
+    return vnew;
+}
+
+// Row (i,j) update from Sg = sum_k (b2 x^2 + b1 x) (PAPER.md:432-448 via I1):
+//   W = Sg + sum_k b0 - n lam,  t = h + p - W,  lam' = kappa t  (kappa = rho2/(rho1 + n rho2)),
+//   zeta' = lam' - lam,  1'z = W + n lam',  h' = min(c, 1'z - p),  p' = p + h' - 1'z.
+struct RowOut {
+    double lam, zeta, h, p;   // new values
+    double r2, r3, s1, s2;    // check terms: |z - g|, |h - 1'z|, max_k |dz|, |dh|
+};
+__device__ __forceinline__ RowOut row_update(double Sg, double sb0, double lam_e, double p_e,
+                                             double h_o, double zeta_o, double c, double nd,
+                                             const double* rho, double dgmax, double dgmin) {
+    RowOut o;
+    const double W = (Sg + sb0) - nd * lam_e;
+    const double kap = rho[1] / (rho[0] + nd * rho[1]);
+    const double t = (h_o + p_e) - W;
+    o.lam = kap * t;
+    o.zeta = o.lam - lam_e;
+    const double oneTz = W + nd * o.lam;
+    o.h = fmin(c, oneTz - p_e);
+    o.p = (p_e + o.h) - oneTz;
+    const double dz = o.zeta - zeta_o;
+    o.r2 = fabs(o.zeta);
+    o.r3 = fabs(o.h - oneTz);
+    o.s1 = fmax(dgmax + dz, -(dgmin + dz));
+    o.s2 = fabs(o.h - h_o);
+    return o;
+}
+
+// rho adaptation + termination at a check (readings
+// G10-G12).  t = {r1..r4, raw sigma terms}.  Returns conv; writes rho_new, f.
+__device__ __forceinline__ int check_decide(const DParams& P, const double* rho, const double* t,
+                                            double* rho_new, double* f, double* r_out,
+                                            double* s_out, double* fac_out, double* s123) {
+    const double s1 = rho[0] * t[4], s2 = rho[1] * t[5], s3 = rho[2] * t[6];
+    const double r = fmax(fmax(t[0], t[1]), fmax(t[2], t[3]));
+    const double sg = fmax(s1, fmax(s2, s3));
+    const int conv = (r < P.r_bar) && (sg < P.sigma_bar);
+    double fac = 1.0;
+    for (int l = 0; l < 4; ++l) {
+        rho_new[l] = rho[l];
+        f[l] = 1.0;
+    }
+    if (!conv && P.adapt) {
+        const double thr_hi = P.hi_ratio * P.r_bar / P.sigma_bar;
+        const double thr_lo = P.lo_ratio * P.r_bar / P.sigma_bar;
+        const double ratio = (sg > 0.0) ? r / sg : INFINITY;  // reading G12
+        int dir = 0;
+        if (ratio > thr_hi) dir = 1;
+        else if (ratio < thr_lo) dir = -1;
+        if (dir != 0) {
+            for (int l = 0; l < 4; ++l) {
+                const double old = rho[l];
+                const double nw = dir > 0 ? old * P.tau : old / P.tau;
+                rho_new[l] = nw;
+                f[l] = P.rescale ? old / nw : 1.0;
+            }
+            fac = dir > 0 ? P.tau : 1.0 / P.tau;
+        }
+    }
+    *r_out = r;
+    *s_out = sg;
+    *fac_out = fac;
+    s123[0] = s1;
+    s123[1] = s2;
+    s123[2] = s3;
+    return conv;
+}
+
+__device__ __forceinline__ void write_hist(double* h, long long it1, double r, double sg,
+                                           const double* rho, const double* t, const double* s123,
+                                           int conv, double fac) {
+    h[0] = (double)it1;
+    h[1] = r;
+    h[2] = sg;
+    for (int l = 0; l < 4; ++l) h[3 + l] = rho[l];
+    for (int l = 0; l < 4; ++l) h[7 + l] = t[l];
+    h[11] = s123[0];
+    h[12] = s123[1];
+    h[13] = s123[2];
+    h[14] = conv;
+    h[15] = fac;
+}
+
 // ------------------------------------------------------- global finalisation
 // Consumes the per-rank aggregates (rank order), computes (6c), the residuals
 // r / sigma, the termination test and the rho adaptation, and writes the next
@@ -135,28 +277,11 @@ __device__ void finalize_global(const KArgs& a, const double* agg, int world, lo
             t[5] = fmax(t[5], g[3 * MAXM + 4]);
             t[6] = fmax(t[6], g[3 * MAXM + 5]);
         }
-        const double* rho = cin.rho;
-        const double s1 = rho[0] * t[4], s2 = rho[1] * t[5], s3 = rho[2] * t[6];
-        const double r = fmax(fmax(t[0], t[1]), fmax(t[2], t[3]));
-        const double sg = fmax(s1, fmax(s2, s3));
-        const int conv = (r < P.r_bar) && (sg < P.sigma_bar);
-        double fac = 1.0;
-        if (!conv && P.adapt) {
-            const double thr_hi = P.hi_ratio * P.r_bar / P.sigma_bar;
-            const double thr_lo = P.lo_ratio * P.r_bar / P.sigma_bar;
-            const double ratio = (sg > 0.0) ? r / sg : INFINITY;  // reading G12
-            int dir = 0;
-            if (ratio > thr_hi) dir = 1;
-            else if (ratio < thr_lo) dir = -1;
-            if (dir != 0) {
-                for (int l = 0; l < 4; ++l) {
-                    const double old = rho[l];
-                    const double nw = dir > 0 ? old * P.tau : old / P.tau;
-                    cout.rho[l] = nw;
-                    cout.f[l] = P.rescale ? old / nw : 1.0;
-                }
-                fac = dir > 0 ? P.tau : 1.0 / P.tau;
-            }
+        double rn[4], fl[4], r, sg, fac, s123[3];
+        const int conv = check_decide(P, cin.rho, t, rn, fl, &r, &sg, &fac, s123);
+        for (int l = 0; l < 4; ++l) {
+            cout.rho[l] = rn[l];
+            cout.f[l] = fl[l];
         }
         cout.r = r;
         cout.sigma = sg;
@@ -167,19 +292,9 @@ __device__ void finalize_global(const KArgs& a, const double* agg, int world, lo
             cout.done = 1;
         }
         if (conv && P.stop_on_conv) cout.done = 1;
-        if (a.hist && a.hist_cap > 0) {
-            double* h = a.hist + (size_t)(cin.checks % a.hist_cap) * HCOLS;
-            h[0] = (double)(it + 1);
-            h[1] = r;
-            h[2] = sg;
-            for (int l = 0; l < 4; ++l) h[3 + l] = rho[l];
-            for (int l = 0; l < 4; ++l) h[7 + l] = t[l];
-            h[11] = s1;
-            h[12] = s2;
-            h[13] = s3;
-            h[14] = conv;
-            h[15] = fac;
-        }
+        if (a.hist && a.hist_cap > 0)
+            write_hist(a.hist + (size_t)(cin.checks % a.hist_cap) * HCOLS, it + 1, r, sg, cin.rho, t,
+                       s123, conv, fac);
     }
 }
 
@@ -193,29 +308,17 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
                                              double Sg, double dgmax, double dgmin, double* r2,
                                              double* r3, double* s1, double* s2) {
     const long long rix = (long long)i * a.q + j;
-    const double nd = (double)a.n;
-    const double lam_e = __ldcg(a.lam + rix) * cin.f[0];
-    const double p_e = __ldcg(a.p + rix) * cin.f[1];
-    const double h_o = __ldcg(a.h + rix);
-    const double zeta_o = __ldcg(a.zeta + rix);
-    const double* rho = cin.rho;
-    const double W = (Sg + a.sb0[rix]) - nd * lam_e;
-    const double kap = rho[1] / (rho[0] + nd * rho[1]);
-    const double t = (h_o + p_e) - W;
-    const double lam_n = kap * t;
-    const double zeta_n = lam_n - lam_e;
-    const double oneTz = W + nd * lam_n;
-    const double h_n = fmin(a.c[i], oneTz - p_e);
-    const double p_n = (p_e + h_n) - oneTz;
-    __stcg(a.lam + rix, lam_n);
-    __stcg(a.zeta + rix, zeta_n);
-    __stcg(a.h + rix, h_n);
-    __stcg(a.p + rix, p_n);
-    const double dz = zeta_n - zeta_o;
-    *r2 = fabs(zeta_n);
-    *r3 = fabs(h_n - oneTz);
-    *s1 = fmax(dgmax + dz, -(dgmin + dz));
-    *s2 = fabs(h_n - h_o);
+    const RowOut o = row_update(Sg, a.sb0[rix], __ldcg(a.lam + rix) * cin.f[0],
+                                __ldcg(a.p + rix) * cin.f[1], __ldcg(a.h + rix),
+                                __ldcg(a.zeta + rix), a.c[i], (double)a.n, cin.rho, dgmax, dgmin);
+    __stcg(a.lam + rix, o.lam);
+    __stcg(a.zeta + rix, o.zeta);
+    __stcg(a.h + rix, o.h);
+    __stcg(a.p + rix, o.p);
+    *r2 = o.r2;
+    *r3 = o.r3;
+    *s1 = o.s1;
+    *s2 = o.s2;
 }
 
 template <int M, int MODE>
@@ -315,56 +418,34 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             }
         }
 
-        // ---- (6a) Gauss-Seidel over sources, per cell
+        // ---- (6a) Gauss-Seidel over sources, then (6e)/(6f), per cell
+        double zl[M], x1nu[M];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            // s, mu of the previous iteration (identity I2) with mu's pending rescale
-            const double s_e = fmax(vv[c], 0.0);
-            const double mu_e = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
-            const bool kk0 = owns_k0 && c == 0;
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double others = 0.0;
-#pragma unroll
-                for (int l = 0; l < M; ++l)
-                    if (l != i) others += (l < i) ? xn[l][c] : xo[l][c];
-                const double phi = ((s_e - others) + yv[c]) + mu_e;
-                const double xoi = xo[i][c];
-                const double b2 = cb2[i][c], b1 = cb1[i][c];
-                // e = theta - b0 = g(x_old) + zeta + lam - b0 (z = g(x) + zeta, I1)
-                const double e = fma(fma(b2, xoi, b1), xoi, zeta_o[i] + lam_e[i]);
-                const double A = 0.5 * rho[0] * b2 * b2;
-                const double B = rho[0] * b2 * b1;
-                double C = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i][c], iq, 0.5 * rho[2]));
-                double D = fma(-rho[0] * b1, e, fma(ca1[i][c], iq, -rho[2] * phi));
-                if (kk0) {
-                    C += 0.5 * rho[3];
-                    D += -rho[3] * (cin.x1[i] + nu_e[i]);
-                }
-                xn[i][c] = quartic_boxmin<MODE>(A, B, C, D, clo[i][c], chi[i][c]);
-            }
+        for (int i = 0; i < M; ++i) {
+            zl[i] = zeta_o[i] + lam_e[i];
+            x1nu[i] = cin.x1[i] + nu_e[i];
         }
-
-        // ---- (6e)/(6f) per cell, row partials of (6b), check terms
         double vn[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const bool valid = c == 0 ? v0 : v1;
-            double sx = 0.0, dx = 0.0;
+            double tca2[M], tca1[M], tcb2[M], tcb1[M], tlo[M], thi[M], txo[M], txn[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                sx += xn[i][c];
-                dx += xn[i][c] - xo[i][c];
+                tca2[i] = ca2[i][c]; tca1[i] = ca1[i][c]; tcb2[i] = cb2[i][c]; tcb1[i] = cb1[i][c];
+                tlo[i] = clo[i][c]; thi[i] = chi[i][c]; txo[i] = xo[i][c];
             }
+            const double s_e = fmax(vv[c], 0.0);
             const double mu_e = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
-            const double s_o = fmax(vv[c], 0.0);
-            const double vnew = (sx - yv[c]) - mu_e;
-            const double s_n = fmax(vnew, 0.0);
+            gs_cell<M, MODE>(tca2, tca1, tcb2, tcb1, tlo, thi, txo, txn, yv[c], s_e, mu_e, zl, rho,
+                             iq, owns_k0 && c == 0, x1nu);
+            const bool valid = c == 0 ? v0 : v1;
+            double r1l = my_r1, s3l = my_s3;
+            const double vnew = cell_tail<M>(txo, txn, yv[c], vv[c], f[2], is_check && valid, r1l, s3l);
+            my_r1 = r1l;
+            my_s3 = s3l;
             vn[c] = valid ? vnew : 0.0;
-            if (is_check && valid) {
-                my_r1 = fmax(my_r1, fabs((s_n - sx) + yv[c]));
-                my_s3 = fmax(my_s3, fabs((s_n - s_o) - dx));
-            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) xn[i][c] = txn[i];
         }
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -533,28 +614,38 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
     if (!s_last) return;
     __threadfence();
 
-    // ---- last CTA: reduce CTA partials in CTA order (warp 0, fixed tree)
-    if (wid == 0) {
-        for (int s = 0; s < XB; ++s) {
-            const bool is_sum = s < MAXM;
-            const bool is_min = s >= 2 * MAXM && s < 3 * MAXM;
-            double v = is_sum ? 0.0 : (is_min ? INFINITY : -INFINITY);
-            if (s >= 3 * MAXM) v = 0.0;
-            for (int g = lane; g < a.G; g += 32) {
-                const double t = __ldcg(a.cta_part + (size_t)g * XB + s);
-                v = is_sum ? v + t : (is_min ? fmin(v, t) : fmax(v, t));
-            }
-            v = is_sum ? warp_sum(v) : (is_min ? warp_min(v) : warp_max(v));
-            if (lane == 0) a.xsend[s] = v;
+    // ---- last CTA: reduce the G CTA partials; lane = slot, warp w takes
+    // CTAs g = w, w + nw, ... (fixed assignment => deterministic), then
+    // thread s < XB combines the warps in order.
+    {
+        const int s = lane;  // XB == 32 slots
+        const bool is_sum = s < MAXM;
+        const bool is_min = s >= 2 * MAXM && s < 3 * MAXM;
+        const double ident = is_sum ? 0.0 : (is_min ? INFINITY : (s >= 3 * MAXM ? 0.0 : -INFINITY));
+        double v = ident;
+        for (int g = wid; g < a.G; g += nw) {
+            const double t = __ldcg(a.cta_part + (size_t)g * XB + s);
+            v = is_sum ? v + t : (is_min ? fmin(v, t) : fmax(v, t));
         }
+        __shared__ double wred[16][XB];
+        wred[wid][s] = v;
+        __syncthreads();
+        if (tid < XB) {
+            double r = ident;
+            for (int w = 0; w < nw; ++w) {
+                const double t = wred[w][tid];
+                r = is_sum ? r + t : (is_min ? fmin(r, t) : fmax(r, t));
+            }
+            acc[tid] = r;
+        }
+        __syncthreads();
     }
-    __syncthreads();
+    if (tid < XB) a.xsend[tid] = acc[tid];
     if (tid == 0) {
         *a.glob_cnt = 0;
         if (a.world == 1) {
-            __threadfence();
             Ctrl& cout = a.ctrl[(it + 1) & 1];
-            finalize_global(a, a.xsend, 1, it, cin, cout, is_check);
+            finalize_global(a, acc, 1, it, cin, cout, is_check);
             __threadfence();
             *(volatile long long*)a.iter = it + 1;
         }

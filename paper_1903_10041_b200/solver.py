@@ -71,6 +71,16 @@ class AdmmSolver:
         _lib.admm_set_problem(self.ctx, *self._keep)
         self._keep = None
 
+    def set_problem_packed(self, f, g, lo, hi, y, c):
+        """Same as set_problem with the coefficient blocks already packed as
+        f = [3][m][q][n] (a2,a1,a0) and g = [3][m][q][n] (b2,b1,b0) -- no
+        host-side staging copy (e.g. pinned torch tensors)."""
+        _lib.admm_set_problem(self.ctx, f, g, lo, hi, y, c)
+
+    def reset(self):
+        """Back to the initial state (reading G19) without re-sending data."""
+        _lib.admm_reset(self.ctx)
+
     def set_params(self, **kw):
         p = _lib.admm_get_params(self.ctx)
         for k, v in kw.items():
