@@ -422,7 +422,7 @@ struct admm_ctx {
     long long* h_iter = nullptr;  // pinned
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
     bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
-    int last_engine = 0;          // 1 streaming, 2 persistent (last call)
+    int last_engine = 0;          // 1 streaming, 2 persistent grid, 3 persistent cluster
 };
 
 namespace {
@@ -636,28 +636,131 @@ admm_status launch_persist(admm_ctx* ctx, persist_fn fn, const PPlan& pl) {
     return ADMM_OK;
 }
 
+typedef void (*cluster_fn)(KArgs, CArgs);
+
+cluster_fn pick_cluster(int m, int mode) {
+#define S(MM)                                                                                  \
+    if (m == MM) return mode == BOX_EXACT ? persist_cluster_kernel<MM, BOX_EXACT>              \
+                                          : persist_cluster_kernel<MM, BOX_PROJECT>;
+    S(1) S(2) S(3) S(4)
+#undef S
+    return nullptr;
+}
+
+// rows inside clusters of T <= 8 CTAs (see admm_persist.cuh)
+PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
+    PPlan pl;
+    if (ctx->world > 1 || !fn) return pl;
+    const long long n = ctx->n, q = ctx->q;
+    const int sms = ctx->sms;
+    long long T = std::max<long long>((n + 1023) / 1024, q <= sms ? sms / q : 1);
+    T = std::min<long long>(T, (n + 63) / 64);
+    T = std::max<long long>(std::min<long long>(T, 8), 1);
+    long long TC = 0;
+    size_t smem = 0;
+    for (int guard = 0; guard < 16; ++guard) {
+        const long long per = (n + T - 1) / T;
+        TC = 64 * ((per + 63) / 64);
+        T = (n + TC - 1) / TC;
+        smem = (size_t)(7 * ctx->m + 2) * TC * 8;
+        if (smem <= 200 * 1024 && TC <= 1024) break;
+        ++T;
+    }
+    if (T > 8 || TC > 1024 || smem > 200 * 1024) return pl;
+    const long long G = q * T;
+    if (G > 32LL * sms) return pl;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return pl;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3((unsigned)(TC / 2));
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)T;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return pl;
+    }
+    if ((long long)nclusters < q) return pl;
+    pl.ok = true;
+    pl.TC = (int)TC;
+    pl.T = (int)T;
+    pl.G = (int)G;
+    pl.BS = (int)(TC / 2);
+    pl.smem = smem;
+    return pl;
+}
+
+admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
+    CArgs ca;
+    ca.TC = pl.TC;
+    ca.T = pl.T;
+    ca.G = pl.G;
+    ca.cpart = (double*)(ctx->ws + ctx->L.pc);
+    ca.rpart = (double*)(ctx->ws + ctx->L.pr);
+    ca.rowchk = (double*)(ctx->ws + ctx->L.prc);
+    ca.cnt = (unsigned long long*)(ctx->ws + ctx->L.pbar);
+    CKC(cudaMemsetAsync(ca.cnt, 0, 256, ctx->stream));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl.G);
+    cfg.blockDim = dim3((unsigned)pl.BS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.T;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    CKC(cudaLaunchKernelEx(&cfg, fn, ctx->ka, ca));
+    return ADMM_OK;
+}
+
 // run until done or iter_limit, through the graph
 admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "set_problem must be called first");
     admm_status st = ADMM_OK;
-    PPlan pl;
+    PPlan pl, cpl;
     persist_fn pfn = nullptr;
+    cluster_fn cfn = nullptr;
     if (ctx->params.exec_mode != ADMM_EXEC_STREAMING) {
-        pfn = pick_persist(ctx->m, ctx->params.box_mode);
-        pl = plan_persist(ctx, pfn);
-        if (!pl.ok && ctx->params.exec_mode == ADMM_EXEC_PERSISTENT)
+        const char* gm = getenv("ADMM_PERSIST_GRID");  // force the grid-barrier variant
+        if (!(gm && gm[0] == '1')) {
+            cfn = pick_cluster(ctx->m, ctx->params.box_mode);
+            cpl = plan_cluster(ctx, cfn);
+        }
+        if (!cpl.ok) {
+            pfn = pick_persist(ctx->m, ctx->params.box_mode);
+            pl = plan_persist(ctx, pfn);
+        }
+        if (!pl.ok && !cpl.ok && ctx->params.exec_mode == ADMM_EXEC_PERSISTENT)
             return fail(ctx, ADMM_ERR_INVALID, "problem does not fit the persistent engine");
     }
-    if (!pl.ok) {
+    if (!pl.ok && !cpl.ok) {
         st = build_graph(ctx);
         if (st != ADMM_OK) return st;
     }
-    ctx->last_engine = pl.ok ? 2 : 1;
+    ctx->last_engine = cpl.ok ? 3 : (pl.ok ? 2 : 1);
     upload_params(ctx, iter_limit, stop_on_conv);
     clear_done_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka);
     const long long start = ctx->iter_host;
     CKC(cudaEventRecord(ctx->e0, ctx->stream));
-    if (pl.ok) {
+    if (cpl.ok) {
+        st = launch_cluster(ctx, cfn, cpl);
+        if (st != ADMM_OK) return st;
+    } else if (pl.ok) {
         st = launch_persist(ctx, pfn, pl);
         if (st != ADMM_OK) return st;
     } else if (ctx->no_graph) {

@@ -46,7 +46,10 @@ def compare_states(P, So, Sg, tol=1e-9):
     return worst
 
 
-ENGINES = [1, 2]  # ADMM_EXEC_STREAMING, ADMM_EXEC_PERSISTENT
+# streaming sweep + graph while loop; persistent with rows in clusters; persistent
+# with a grid barrier per iteration (forced through ADMM_PERSIST_GRID=1)
+ENGINES = ["stream", "cluster", "grid"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, 0: 0}
 
 
 def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_iter=None,
@@ -57,7 +60,13 @@ def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_it
                      r_bar=params["r_bar"], sigma_bar=params["sigma_bar"],
                      check_every=params["check_every"], adapt_rho=params["adapt_rho"],
                      rescale_duals=params["rescale_duals"], box_mode=params["box_mode"],
-                     exec_mode=engine)
+                     exec_mode=_EXEC[engine])
+    import os
+
+    if engine == "grid":
+        os.environ["ADMM_PERSIST_GRID"] = "1"
+    else:
+        os.environ.pop("ADMM_PERSIST_GRID", None)
     s.set_problem(P)
     info = None
     if mode == "iterate":
@@ -68,6 +77,7 @@ def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_it
     x, x1, sol = s.solution()
     hist = s.history()
     s.close()
+    os.environ.pop("ADMM_PERSIST_GRID", None)
     return S, sol if info is None else {**sol, **info}, hist
 
 
