@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libadmm_b200.so")
+SO_PATH = os.environ.get("ADMM_SO") or os.path.join(_HERE, "libadmm_b200.so")  # ADMM_SO: dev builds
 
 if not os.path.exists(SO_PATH):
     raise ImportError(

@@ -25,6 +25,7 @@
 #include "admm.h"
 #include "admm_kernels.cuh"
 #include "admm_persist.cuh"
+#include "admm_onchip.cuh"
 
 using namespace admm_dev;
 
@@ -38,7 +39,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, total;
+        prc, pbar, pub, xraw, total;
 };
 
 int pick_bs(long long n) {
@@ -80,6 +81,8 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.pr = take(2 * GP * 2 * 8);
     L.prc = take(2 * (size_t)m * std::min<size_t>(q, GP) * 4 * 8);
     L.pbar = take(64 * 4);
+    L.pub = take((size_t)PUB_BUFS * m * std::min<size_t>(q, GP) * 8);
+    L.xraw = take(2 * (size_t)m * std::min<size_t>(q, GP) * 8);
     L.total = o;
     return L;
 }
@@ -647,56 +650,64 @@ cluster_fn pick_cluster(int m, int mode) {
     return nullptr;
 }
 
-// rows inside clusters of T <= 8 CTAs (see admm_persist.cuh)
+// rows inside clusters of T <= 16 CTAs (see admm_onchip.cuh): one CTA per SM,
+// at most 16 bulk warps (usually one cell per thread) + the consensus warp.
+// Candidate tile counts: the one that spreads the rows over the SMs, then
+// fewer (when q*T CTAs do not fit, e.g. 3 x 50 > 148), then more (when a
+// long row does not fit the shared memory of T CTAs).
 PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     PPlan pl;
     if (ctx->world > 1 || !fn) return pl;
     const long long n = ctx->n, q = ctx->q;
     const int sms = ctx->sms;
-    long long T = std::max<long long>((n + 1023) / 1024, q <= sms ? sms / q : 1);
-    T = std::min<long long>(T, (n + 63) / 64);
-    T = std::max<long long>(std::min<long long>(T, 8), 1);
-    long long TC = 0;
-    size_t smem = 0;
-    for (int guard = 0; guard < 16; ++guard) {
-        const long long per = (n + T - 1) / T;
-        TC = 64 * ((per + 63) / 64);
-        T = (n + TC - 1) / TC;
-        smem = (size_t)(7 * ctx->m + 2) * TC * 8;
-        if (smem <= 200 * 1024 && TC <= 1024) break;
-        ++T;
-    }
-    if (T > 8 || TC > 1024 || smem > 200 * 1024) return pl;
-    const long long G = q * T;
-    if (G > 32LL * sms) return pl;
-    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess) {
+    if (q * 1LL > 32LL * sms) return pl;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
         cudaGetLastError();
+    long long T0 = std::max<long long>(1, std::min<long long>(ONCHIP_MAX_T, (sms + q - 1) / q));
+    T0 = std::min<long long>(T0, std::max<long long>(1, n / 32));
+    std::vector<long long> cand;
+    for (long long T = T0; T >= 1; --T) cand.push_back(T);
+    for (long long T = T0 + 1; T <= ONCHIP_MAX_T; ++T) cand.push_back(T);
+    for (long long T : cand) {
+        const long long TC = (n + T - 1) / T;
+        if ((n + TC - 1) / TC != T) continue;  // no empty tile
+        const size_t smem = (size_t)(7 * ctx->m + 2) * TC * 8;
+        if (smem > 200 * 1024 || TC > 4 * 512) continue;
+        const long long G = q * T;
+        if (G > 32LL * sms) continue;
+        const int nbw = (int)std::min<long long>(16, (TC + 31) / 32);
+        const int BS = (nbw + 1) * 32;
+        if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)G);
+        cfg.blockDim = dim3((unsigned)BS);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)T;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if ((long long)nclusters < q) continue;  // all CTAs must be co-resident
+        pl.ok = true;
+        pl.TC = (int)TC;
+        pl.T = (int)T;
+        pl.G = (int)G;
+        pl.BS = BS;
+        pl.smem = smem;
         return pl;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3((unsigned)(TC / 2));
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)T;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return pl;
-    }
-    if ((long long)nclusters < q) return pl;
-    pl.ok = true;
-    pl.TC = (int)TC;
-    pl.T = (int)T;
-    pl.G = (int)G;
-    pl.BS = (int)(TC / 2);
-    pl.smem = smem;
     return pl;
 }
 
@@ -705,25 +716,31 @@ admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
     ca.TC = pl.TC;
     ca.T = pl.T;
     ca.G = pl.G;
-    ca.cpart = (double*)(ctx->ws + ctx->L.pc);
+    ca.pub = (double*)(ctx->ws + ctx->L.pub);
+    ca.xraw = (double*)(ctx->ws + ctx->L.xraw);
     ca.rpart = (double*)(ctx->ws + ctx->L.pr);
     ca.rowchk = (double*)(ctx->ws + ctx->L.prc);
     ca.cnt = (unsigned long long*)(ctx->ws + ctx->L.pbar);
     CKC(cudaMemsetAsync(ca.cnt, 0, 256, ctx->stream));
+    const long long nslots = (long long)PUB_BUFS * ctx->m * ctx->q;
+    pub_reset_kernel<<<(unsigned)std::min<long long>(64, (nslots + 255) / 256), 256, 0, ctx->stream>>>(
+        ca.pub, nslots);
+    CKC(cudaGetLastError());
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pl.smem) != cudaSuccess)
+        return fail(ctx, ADMM_ERR_CUDA, "cluster kernel: shared memory attribute");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl.G);
     cfg.blockDim = dim3((unsigned)pl.BS);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)pl.T;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeCooperative;
-    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 1;
     CKC(cudaLaunchKernelEx(&cfg, fn, ctx->ka, ca));
     return ADMM_OK;
 }
@@ -1311,3 +1328,9 @@ const char* admm_build_info(void) {
 }
 
 }  // extern "C"
+
+#ifdef ADMM_PHASE_PROF
+extern "C" int admm_debug_phase(unsigned long long* out16) {
+    return cudaMemcpyFromSymbol(out16, admm_dev::g_phase, sizeof(admm_dev::g_phase)) == cudaSuccess ? 0 : 1;
+}
+#endif
