@@ -39,7 +39,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, pub, xraw, total;
+        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, total;
 };
 
 int pick_bs(long long n) {
@@ -47,6 +47,8 @@ int pick_bs(long long n) {
     long long bs = ((need + 31) / 32) * 32;
     return (int)std::max(32LL, std::min(512LL, bs));
 }
+
+constexpr size_t ONCHIP_PREP_MAX_ELEMS = (size_t)1 << 23;  // m*q*n_pad of the largest on-chip problem
 
 Layout make_layout(int m, long long n, long long q, int sms) {
     Layout L{};
@@ -83,6 +85,12 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.pbar = take(64 * 4);
     L.pub = take((size_t)PUB_BUFS * m * std::min<size_t>(q, GP) * 8);
     L.xraw = take(2 * (size_t)m * std::min<size_t>(q, GP) * 8);
+    // prepared constants for the on-chip engine (only for problems that can be on chip)
+    const bool onchip_sized = (size_t)m * q * n_pad <= ONCHIP_PREP_MAX_ELEMS;
+    L.bq = take(onchip_sized ? E : 8);
+    L.ib2s = take(onchip_sized ? E : 8);
+    L.chk = take(3 * CHK_SLOTS * 8);
+    L.gbound = take(MAXM * 8);
     L.total = o;
     return L;
 }
@@ -127,6 +135,36 @@ __global__ void validate_kernel(int m, long long q, long long n, long long n_pad
     }
     if (blockIdx.x == 0 && threadIdx.x < m && isnan(c[threadIdx.x]))
         atomicMin(flag, (6ull << 56) | (unsigned long long)threadIdx.x);
+}
+
+// per source i: max over (j,k) of |b2 x^2 + b1 x| over the box (x in [lo, hi]),
+// as order-preserving keys (fixed-point scale of the on-chip row sums)
+__global__ void gbound_kernel(int m, long long q, long long n, long long n_pad, const double* b2,
+                              const double* b1, const double* lo, const double* hi,
+                              unsigned long long* out) {
+    const long long NE = (long long)m * q * n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t0 = blockIdx.x * (long long)blockDim.x; t0 < NE; t0 += stride) {
+        const long long t = t0 + threadIdx.x;
+        double g = 0.0;
+        int i = (int)(t0 / (q * n));
+        if (t < NE) {
+            const long long k = t % n, ij = t / n;
+            i = (int)(ij / q);
+            const long long e = ij * n_pad + k;
+            const double X = fmax(fabs(lo[i * n_pad + k]), fabs(hi[i * n_pad + k]));
+            g = fma(b2[e] * X, X, fabs(b1[e]) * X);
+            if (isnan(g)) g = INFINITY;
+        }
+        // warps are source-uniform except at source boundaries: per-lane atomics there
+        const int i0 = __shfl_sync(0xffffffffu, i, 0);
+        if (__all_sync(0xffffffffu, i == i0)) {
+            g = warp_max(g);
+            if ((threadIdx.x & 31) == 0) atomicMax(out + i0, okey(g));
+        } else if (t < NE) {
+            atomicMax(out + i, okey(g));
+        }
+    }
 }
 
 // init (reading G19): x = clamp(midpoint) or clamp(0); v = s = max(0, sum_i x - y)
@@ -426,6 +464,8 @@ struct admm_ctx {
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
     bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
     int last_engine = 0;          // 1 streaming, 2 persistent grid, 3 persistent cluster
+    bool prep_ok = false;         // bq / ib2s / fixed-point scales valid for the cluster engine
+    double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
 };
 
 namespace {
@@ -576,7 +616,7 @@ persist_fn pick_persist(int m, int mode) {
 
 struct PPlan {
     bool ok = false;
-    int TC = 0, T = 0, G = 0, BS = 0;
+    int TC = 0, T = 0, G = 0, BS = 0, TC0 = 0;
     size_t smem = 0;
 };
 
@@ -652,31 +692,39 @@ cluster_fn pick_cluster(int m, int mode) {
 
 // rows inside clusters of T <= 16 CTAs (see admm_onchip.cuh): one CTA per SM,
 // at most 16 bulk warps (usually one cell per thread) + the consensus warp.
+// Tile 0 (which also runs the consensus chain) gets TC0 ~ frac * n/T cells.
 // Candidate tile counts: the one that spreads the rows over the SMs, then
 // fewer (when q*T CTAs do not fit, e.g. 3 x 50 > 148), then more (when a
 // long row does not fit the shared memory of T CTAs).
 PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     PPlan pl;
-    if (ctx->world > 1 || !fn) return pl;
+    if (ctx->world > 1 || !fn || !ctx->prep_ok) return pl;
     const long long n = ctx->n, q = ctx->q;
     const int sms = ctx->sms;
-    if (q * 1LL > 32LL * sms) return pl;
+    if (q > 32LL * sms) return pl;
     if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
         cudaGetLastError();
+    double frac = 0.6;
+    if (const char* e = getenv("ADMM_TILE0_FRAC")) frac = atof(e);
     long long T0 = std::max<long long>(1, std::min<long long>(ONCHIP_MAX_T, (sms + q - 1) / q));
     T0 = std::min<long long>(T0, std::max<long long>(1, n / 32));
     std::vector<long long> cand;
     for (long long T = T0; T >= 1; --T) cand.push_back(T);
     for (long long T = T0 + 1; T <= ONCHIP_MAX_T; ++T) cand.push_back(T);
     for (long long T : cand) {
-        const long long TC = (n + T - 1) / T;
-        if ((n + TC - 1) / TC != T) continue;  // no empty tile
-        const size_t smem = (size_t)(7 * ctx->m + 2) * TC * 8;
-        if (smem > 200 * 1024 || TC > 4 * 512) continue;
+        long long TC0 = n, TC = n;
+        if (T > 1) {
+            TC0 = std::max<long long>(1, std::min<long long>(n - (T - 1), (long long)std::llround(frac * n / T)));
+            TC = (n - TC0 + T - 2) / (T - 1);
+            if (TC0 + (T - 2) * TC >= n) continue;  // last tile would be empty
+        }
+        const long long TCM = std::max(TC0, TC);
+        const size_t smem = (size_t)(9 * ctx->m + 2) * TCM * 8;
+        if (smem > 200 * 1024 || TCM > 4 * 512) continue;
         const long long G = q * T;
         if (G > 32LL * sms) continue;
-        const int nbw = (int)std::min<long long>(16, (TC + 31) / 32);
+        const int nbw = (int)std::min<long long>(16, (TCM + 31) / 32);
         const int BS = (nbw + 1) * 32;
         if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess) {
@@ -701,6 +749,7 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
         }
         if ((long long)nclusters < q) continue;  // all CTAs must be co-resident
         pl.ok = true;
+        pl.TC0 = (int)TC0;
         pl.TC = (int)TC;
         pl.T = (int)T;
         pl.G = (int)G;
@@ -713,18 +762,23 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
 
 admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
     CArgs ca;
+    ca.TC0 = pl.TC0;
     ca.TC = pl.TC;
     ca.T = pl.T;
     ca.G = pl.G;
+    for (int i = 0; i < MAXM; ++i) {
+        ca.fx_scale[i] = ctx->fx_scale[i];
+        ca.fx_inv[i] = ctx->fx_inv[i];
+    }
+    ca.bq = (const double*)(ctx->ws + ctx->L.bq);
+    ca.ib2s = (const double*)(ctx->ws + ctx->L.ib2s);
     ca.pub = (double*)(ctx->ws + ctx->L.pub);
-    ca.xraw = (double*)(ctx->ws + ctx->L.xraw);
-    ca.rpart = (double*)(ctx->ws + ctx->L.pr);
-    ca.rowchk = (double*)(ctx->ws + ctx->L.prc);
+    ca.chk = (unsigned long long*)(ctx->ws + ctx->L.chk);
     ca.cnt = (unsigned long long*)(ctx->ws + ctx->L.pbar);
     CKC(cudaMemsetAsync(ca.cnt, 0, 256, ctx->stream));
     const long long nslots = (long long)PUB_BUFS * ctx->m * ctx->q;
-    pub_reset_kernel<<<(unsigned)std::min<long long>(64, (nslots + 255) / 256), 256, 0, ctx->stream>>>(
-        ca.pub, nslots);
+    onchip_reset_kernel<<<(unsigned)std::min<long long>(64, (nslots + 255) / 256), 256, 0,
+                          ctx->stream>>>(ca.pub, nslots, ca.chk);
     CKC(cudaGetLastError());
     if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pl.smem) != cudaSuccess)
@@ -1077,6 +1131,40 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             snprintf(buf, sizeof buf, "%s at (i=%lld)", kind_msg(kind), t);
         }
         return fail(ctx, (kind == 2 || kind == 3) ? ADMM_ERR_NONCONVEX : ADMM_ERR_INVALID, buf);
+    }
+    // on-chip engine: prepared constants and the fixed-point scales of the row sums
+    ctx->prep_ok = false;
+    if ((size_t)ctx->m * ctx->q * ctx->n_pad <= ONCHIP_PREP_MAX_ELEMS) {
+        const long long NE = (long long)ctx->m * ctx->q * ctx->n_pad;
+        prep_kernel<<<grid_for(NE, 256, ctx->sms), 256, 0, ctx->stream>>>(
+            NE, a.b2, a.b1, (double*)(ctx->ws + ctx->L.bq), (double*)(ctx->ws + ctx->L.ib2s));
+        CKC(cudaGetLastError());
+        unsigned long long* gb = (unsigned long long*)(ctx->ws + ctx->L.gbound);
+        CKC(cudaMemsetAsync(gb, 0, MAXM * 8, ctx->stream));
+        gbound_kernel<<<grid_for(blk, 256, ctx->sms), 256, 0, ctx->stream>>>(
+            ctx->m, ctx->q, ctx->n, ctx->n_pad, a.b2, a.b1, a.lo, a.hi, gb);
+        CKC(cudaGetLastError());
+        unsigned long long keys[MAXM];
+        CKC(cudaMemcpyAsync(keys, gb, MAXM * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CKC(cudaStreamSynchronize(ctx->stream));
+        bool ok = true;
+        for (int i = 0; i < ctx->m; ++i) {
+            const unsigned long long k = keys[i];
+            unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+            double gbv;
+            std::memcpy(&gbv, &u, 8);
+            const double G = (double)ctx->n * gbv;  // bound on |sum_k (b2 x^2 + b1 x)|
+            if (!(G < 1e300)) {
+                ok = false;
+                break;
+            }
+            int E = 0;
+            if (G > 0.0) E = 62 - (int)std::ceil(std::log2(G));
+            E = std::max(-1000, std::min(1000, E));
+            ctx->fx_scale[i] = std::ldexp(1.0, E);
+            ctx->fx_inv[i] = std::ldexp(1.0, -E);
+        }
+        ctx->prep_ok = ok;
     }
     admm_status is = init_state(ctx);
     if (is != ADMM_OK) return is;

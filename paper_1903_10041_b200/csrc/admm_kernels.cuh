@@ -117,15 +117,55 @@ __device__ __forceinline__ void gs_cell(const double* ca2, const double* ca1, co
         const double xoi = xo[i];
         const double b2 = cb2[i], b1 = cb1[i];
         const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
-        const double A = 0.5 * rho[0] * b2 * b2;
-        const double B = rho[0] * b2 * b1;
         double C = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i], iq, 0.5 * rho[2]));
         double D = fma(-rho[0] * b1, e, fma(ca1[i], iq, -rho[2] * phi));
         if (k0) {
             C += 0.5 * rho[3];
             D += -rho[3] * x1nu[i];
         }
-        xn[i] = quartic_boxmin<MODE>(A, B, C, D, clo[i], chi[i]);
+        if (b2 != 0.0) {
+            // A = rho1 b2^2 / 2, B = rho1 b2 b1: b = 3B/4A, c = C/2A, d = D/4A
+            const double ia2 = rcp_nr(rho[0] * b2 * b2);  // 1 / 2A
+            xn[i] = quartic_core<MODE>(1.5 * (rho[0] * b2 * b1) * ia2, C * ia2, 0.5 * D * ia2, C, D,
+                                       clo[i], chi[i]);
+        } else {
+            xn[i] = clampd(-D * rcp_nr(2.0 * C), clo[i], chi[i]);  // A = B = 0: quadratic
+        }
+    }
+}
+
+// Same update from per-element constants prepared once per problem (on-chip
+// engines): a2q = a2/q, a1q = a1/q, bq = 1.5 b1/b2 (= b, independent of rho),
+// ib2s = 1/b2^2 (0 when b2 = 0).  R = {rho1, rho3, rho4, 1/rho1}.
+template <int M, int MODE>
+__device__ __forceinline__ void gs_cell_prep(const double* a2q, const double* a1q, const double* cb2,
+                                             const double* cb1, const double* bq, const double* ib2s,
+                                             const double* clo, const double* chi, const double* xo,
+                                             double* xn, double y, double s_e, double mu_e,
+                                             const double* zl, const double* R, bool k0,
+                                             const double* x1nu) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double others = 0.0;
+#pragma unroll
+        for (int l = 0; l < M; ++l)
+            if (l != i) others += (l < i) ? xn[l] : xo[l];
+        const double phi = ((s_e - others) + y) + mu_e;
+        const double xoi = xo[i];
+        const double b2 = cb2[i], b1 = cb1[i];
+        const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
+        double C = fma(0.5 * R[0], fma(b1, b1, -2.0 * b2 * e), a2q[i] + 0.5 * R[1]);
+        double D = fma(-R[0] * b1, e, fma(-R[1], phi, a1q[i]));
+        if (k0) {
+            C += 0.5 * R[2];
+            D += -R[2] * x1nu[i];
+        }
+        if (b2 != 0.0) {
+            const double ia2 = ib2s[i] * R[3];  // 1 / 2A = 1 / (rho1 b2^2)
+            xn[i] = quartic_core<MODE>(bq[i], C * ia2, 0.5 * D * ia2, C, D, clo[i], chi[i]);
+        } else {
+            xn[i] = clampd(-D * rcp_nr(2.0 * C), clo[i], chi[i]);
+        }
     }
 }
 

@@ -2,16 +2,21 @@
 // for PHEV-sized problems (BASELINE.json configs[0], [1]; Appendix A,
 // Eq. (6a)-(6i), residuals :464-479, adaptive rho :318-324).
 //
-// Scenario row j = one thread-block cluster of T CTAs (tile r holds steps
-// [r*TC, r*TC + ncell)); coefficients, bounds, demand, x and v = s - mu stay
-// in shared memory for the whole call.  Each bulk thread owns (usually) one
-// cell, so the critical path of an iteration is one Gauss-Seidel cell + one
-// block reduction + one cluster barrier + the scalar row update.
+// Scenario row j = one thread-block cluster of T CTAs; tile 0 holds steps
+// [0, TC0), tile r >= 1 holds [TC0 + (r-1) TC, ...).  Coefficients (prepared:
+// a2/q, a1/q, b2, b1, b = 1.5 b1/b2, 1/b2^2), bounds, demand, x and v = s - mu
+// stay in shared memory for the whole call.  Each bulk thread owns (usually)
+// one cell, so an iteration is one Gauss-Seidel cell + one reduction + one
+// cluster barrier + the scalar row update.
 //
-//  * capacity coupling (6b)/(6g)/(6d)/(6i): warp 0 of every CTA stores its
-//    tile partials straight into every cluster-mate's shared memory (DSMEM),
-//    one cluster.sync(), then every CTA of the row performs the identical row
-//    update from the T partials (fixed order => identical values);
+//  * capacity coupling (6b)/(6g)/(6d)/(6i): the row sum sum_k (b2 x^2 + b1 x)
+//    is accumulated in 64-bit fixed point (per-source scale 2^E chosen at
+//    set_problem so that n * max|b2 x^2 + b1 x| over the box < 2^62): a warp
+//    sums with three redux.sync over 21-bit limbs, lane t < T adds the warp
+//    sum into cluster-mate t's accumulator (DSMEM atomic), one cluster.sync,
+//    and every CTA of the row performs the identical row update.  Integer
+//    addition is associative, so the sum is exact up to the per-term rounding
+//    (<= n 2^-63 of the bound) and independent of order: deterministic;
 //  * consensus (6c)/(6h), the only cross-scenario coupling, touches only the
 //    k = 0 cell.  Tile-0 CTAs carry one extra "consensus warp": at the start
 //    of iteration t it reads the q contributions of iteration t-1 (one L2
@@ -22,10 +27,13 @@
 //    for the consensus; four rotating buffers make the reset race-free: when
 //    a consensus warp has observed every contribution of iteration t-1, every
 //    CTA has passed the row barrier of t-2, so nobody still reads the buffer
-//    of t-3 = t+1 (mod 4);
-//  * residual checks (every check_every): one counter barrier over all CTAs
-//    (release add / acquire poll), after which every CTA reduces the same
-//    published maxima and takes the same termination / rho decision.
+//    of t-3 = t+1 (mod 4).  Tile 0 gets fewer cells (TC0 < TC)
+//    so the k = 0 chain is not starved of issue slots by its bulk warps;
+//  * residual checks (every check_every): every term is a max (or min),
+//    combined with order-independent atomics on order-preserving integer keys
+//    (DSMEM for the row terms, global for the grid terms), one counter
+//    barrier, one round trip to read the combined slots; every CTA takes the
+//    same termination / rho decision.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -35,8 +43,9 @@ namespace admm_dev {
 
 constexpr unsigned long long PUB_EMPTY = 0xFFF4DEADBEEF0001ull;  // sNaN payload: never computed
 constexpr int PUB_BUFS = 4;
-constexpr int ONCHIP_MAX_WARPS = 17;  // 16 bulk warps + 1 consensus warp
-constexpr int ONCHIP_MAX_T = 16;      // tiles (CTAs) per cluster
+constexpr int ONCHIP_MAX_WARPS = 17;     // 16 bulk warps + 1 consensus warp
+constexpr int ONCHIP_MAX_T = 16;         // tiles (CTAs) per cluster
+constexpr int CHK_SLOTS = 6 + 2 * MAXM;  // r1 r2 r3 s1 s2 s3 | max_j x_1 [MAXM] | min_j x_1 [MAXM]
 
 #ifdef ADMM_PHASE_PROF  // development build only: per-phase clock64() totals of CTA 0
 __device__ unsigned long long g_phase[2][8];
@@ -62,15 +71,34 @@ __device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned
     while (ld_acquire(p) < target) {
     }
 }
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_relaxed_u64(double* p, unsigned long long v) {
+__device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// order-preserving map double -> uint64 (max/min of keys = max/min of values)
+__device__ __forceinline__ unsigned long long okey(double x) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+    const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)u);
+}
+
+// exact warp sum of 64-bit two's-complement values (mod 2^64): three 21/21/22-bit
+// limbs, each summed by redux.sync (no carries lost: 32 * 2^22 < 2^32)
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+    const unsigned l0 = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0x1FFFFFull));
+    const unsigned l1 = __reduce_add_sync(0xffffffffu, (unsigned)((v >> 21) & 0x1FFFFFull));
+    const unsigned l2 = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 42));
+    return (unsigned long long)l0 + ((unsigned long long)l1 << 21) + ((unsigned long long)l2 << 42);
+}
 
 // (6c) x1^{(i)} = (1/q_total) sum_j c^{(i,j)} over one publication buffer
 // [M][q] (reading G1: the mean).  Warp-collective; every lane returns the same
@@ -114,19 +142,33 @@ __device__ __forceinline__ void read_consensus(const double* buf, long long q, d
 }
 
 struct CArgs {
-    int TC, T, G;
+    int TC0, TC, T, G;
+    double fx_scale[MAXM], fx_inv[MAXM];  // fixed-point scale 2^E_i of the row sums
+    // prepared per-element constants [m][q][n_pad]: b = 1.5 b1/b2, 1/b2^2 (0 if b2 = 0)
+    const double *bq, *ib2s;
     double *pub;                // [PUB_BUFS][m][q] consensus contributions x_1 - nu (epoch slots)
-    double *xraw;               // [2][m][q]        x_1^{(i,j)} by iteration parity (checks)
-    double *rpart;              // [2][G][2]        per-CTA r1, s3 maxima (check parity)
-    double *rowchk;             // [2][m][q][4]     row check terms r2, r3, s1, s2 (check parity)
+    unsigned long long *chk;    // [3][CHK_SLOTS] check maxima (ordered keys), rotating sets
     unsigned long long *cnt;    // [16] check-barrier arrivals (zeroed per launch)
 };
 
-// fill every publication slot with the sentinel (before each launch)
-__global__ void pub_reset_kernel(double* pub, long long nslots) {
+// before each launch: every publication slot = sentinel, check sets = identities
+__global__ void onchip_reset_kernel(double* pub, long long nslots, unsigned long long* chk) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nslots;
          t += (long long)gridDim.x * blockDim.x)
         pub[t] = __longlong_as_double((long long)PUB_EMPTY);
+    if (blockIdx.x == 0)
+        for (int t = threadIdx.x; t < 3 * CHK_SLOTS; t += blockDim.x)
+            chk[t] = (t % CHK_SLOTS) >= 6 + MAXM ? ~0ull : 0ull;
+}
+
+// prepared constants (once per problem): b = 1.5 b1/b2, 1/b2^2
+__global__ void prep_kernel(long long NE, const double* b2, const double* b1, double* bq, double* ib2s) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NE;
+         t += (long long)gridDim.x * blockDim.x) {
+        const double v2 = b2[t];
+        bq[t] = v2 != 0.0 ? 1.5 * b1[t] / v2 : 0.0;
+        ib2s[t] = v2 != 0.0 ? 1.0 / (v2 * v2) : 0.0;
+    }
 }
 
 template <int M, int MODE>
@@ -134,20 +176,23 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
-    const int TC = p.TC;
-    double* s_a2 = sm;
-    double* s_a1 = s_a2 + M * TC;
-    double* s_b2 = s_a1 + M * TC;
-    double* s_b1 = s_b2 + M * TC;
-    double* s_lo = s_b1 + M * TC;
-    double* s_hi = s_lo + M * TC;
-    double* s_x = s_hi + M * TC;
-    double* s_y = s_x + M * TC;
-    double* s_v = s_y + TC;
+    const int TCM = max(p.TC0, p.TC);  // shared-memory row stride
+    double* s_a2q = sm;
+    double* s_a1q = s_a2q + M * TCM;
+    double* s_b2 = s_a1q + M * TCM;
+    double* s_b1 = s_b2 + M * TCM;
+    double* s_bq = s_b1 + M * TCM;
+    double* s_ib = s_bq + M * TCM;
+    double* s_lo = s_ib + M * TCM;
+    double* s_hi = s_lo + M * TCM;
+    double* s_x = s_hi + M * TCM;
+    double* s_y = s_x + M * TCM;
+    double* s_v = s_y + TCM;
 
-    __shared__ double red[ONCHIP_MAX_WARPS][3 * M + 2];
-    __shared__ double s_part[2][ONCHIP_MAX_T][3 * M];  // [parity][tile], written by mates (DSMEM)
-    __shared__ double s_zl[M], s_x1[M], s_rho[4], s_f[4], s_t[2];
+    __shared__ unsigned long long s_acc[2][M];       // fixed-point row sums, added by mates
+    __shared__ double s_dgp[ONCHIP_MAX_T][2 * M];    // per-tile max / min of dg (checks), by mates
+    __shared__ double s_wred[ONCHIP_MAX_WARPS][2 * M + 2];  // per-warp check maxima
+    __shared__ double s_zl[M], s_x1[M], s_rho[4], s_R[4], s_kap, s_f[4], s_t[2];
     __shared__ int s_flag[2];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -157,8 +202,8 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     const int T = p.T;
     const long long j = blockIdx.x / T;
     const int tile = (int)cluster.block_rank();
-    const int k0 = tile * TC;
-    const int ncell = min(TC, a.n - k0);
+    const int k0 = tile == 0 ? 0 : p.TC0 + (tile - 1) * p.TC;
+    const int ncell = min(tile == 0 ? p.TC0 : p.TC, a.n - k0);
     const long long qn = a.q * (long long)a.n_pad;
     const long long qq = a.q;
     const DParams& P = *a.prm;
@@ -170,20 +215,23 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     const Ctrl& cin = a.ctrl[it0 & 1];
     if (cin.done || it0 >= P.iter_limit) return;  // uniform over the grid
 
-    for (int t = tid; t < M * TC; t += blockDim.x) {
-        const int i = t / TC, c = t - i * TC;
+    const double iq = a.inv_q;
+    for (int t = tid; t < M * TCM; t += blockDim.x) {
+        const int i = t / TCM, c = t - i * TCM;
         const bool ok = c < ncell;
         const long long e = (long long)i * qn + j * a.n_pad + k0 + c;
         const long long bk = (long long)i * a.n_pad + k0 + c;
-        s_a2[t] = ok ? a.a2[e] : 0.0;
-        s_a1[t] = ok ? a.a1[e] : 0.0;
+        s_a2q[t] = ok ? a.a2[e] * iq : 0.0;
+        s_a1q[t] = ok ? a.a1[e] * iq : 0.0;
         s_b2[t] = ok ? a.b2[e] : 0.0;
         s_b1[t] = ok ? a.b1[e] : 0.0;
+        s_bq[t] = ok ? p.bq[e] : 0.0;
+        s_ib[t] = ok ? p.ib2s[e] : 0.0;
         s_lo[t] = ok ? a.lo[bk] : 0.0;
         s_hi[t] = ok ? a.hi[bk] : 0.0;
         s_x[t] = ok ? a.x[e] : 0.0;
     }
-    for (int c = tid; c < TC; c += blockDim.x) {
+    for (int c = tid; c < TCM; c += blockDim.x) {
         const bool ok = c < ncell;
         const double vv = ok ? a.v[j * a.n_pad + k0 + c] : 0.0;
         s_y[c] = ok ? a.y[j * a.n_pad + k0 + c] : 0.0;
@@ -202,6 +250,8 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
         r_sb0 = a.sb0[rix];
         s_zl[tid] = r_zeta + r_lam;
         s_x1[tid] = cin.x1[tid];
+        s_acc[0][tid] = 0ull;
+        s_acc[1][tid] = 0ull;
     }
     // consensus warp (tile 0), lane i < M: nu, x1, x_1 and the last contribution of source i
     double c_nu = 0.0, c_x1 = 0.0, c_x0 = 0.0, c_pub = 0.0, c_fnu = 1.0;
@@ -212,18 +262,30 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
         c_nu = nu * cin.f[3];
         c_x1 = cin.x1[lane];
     }
-    if (tid < 4) {
-        s_rho[tid] = cin.rho[tid];
-        s_f[tid] = 1.0;
+    if (tid == 0) {
+        for (int l = 0; l < 4; ++l) {
+            s_rho[l] = cin.rho[l];
+            s_f[l] = 1.0;
+        }
+        s_R[0] = cin.rho[0];
+        s_R[1] = cin.rho[2];
+        s_R[2] = cin.rho[3];
+        s_R[3] = 1.0 / cin.rho[0];
+        s_kap = cin.rho[1] / (cin.rho[0] + nd * cin.rho[1]);
+    }
+    double fxs[M], fxi[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        fxs[i] = p.fx_scale[i];
+        fxi[i] = p.fx_inv[i];
     }
     double l_r = cin.r, l_sigma = cin.sigma;
     int l_status = cin.status, l_checks = cin.checks, l_err = cin.err, l_done = 0;
-    const double iq = a.inv_q;
     const int ce = P.check_every;
     unsigned long long nchk = 0;
     bool x1_known = true;  // consensus warp: c_x1 holds x1 of the previous iteration
     __syncthreads();
-    cluster.sync();  // mates' shared memory is live before any DSMEM store
+    cluster.sync();  // mates' shared memory is live before any DSMEM access
 #ifdef ADMM_PHASE_PROF
     const bool prof_on = blockIdx.x == 0 && (tid == 0 || tid == nbt);
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last = clock64();
@@ -236,17 +298,18 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
         const int par = (int)(it & 1);
         const bool is_check = (until_chk == 0);
         until_chk = is_check ? ce - 1 : until_chk - 1;
-        double rho[4];
+        double R[4];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) rho[l] = s_rho[l];
+        for (int l = 0; l < 4; ++l) R[l] = s_R[l];
         double zl[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) zl[i] = s_zl[i];
 
-        double Sg[M], dgx[M], dgn[M];
+        double dgx[M], dgn[M];
+        long long fx[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            Sg[i] = 0.0;
+            fx[i] = 0;
             dgx[i] = -INFINITY;
             dgn[i] = INFINITY;
         }
@@ -255,27 +318,30 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
             // ---- bulk cells: every cell of the tile except the consensus cell k = 0
             for (int cc = tid; cc < ncell; cc += nbt) {
                 if (k0 + cc == 0) continue;
-                double ca2[M], ca1[M], cb2[M], cb1[M], clo[M], chi[M], xo[M], xn[M], dummy[M];
+                double a2q[M], a1q[M], cb2[M], cb1[M], bq[M], ib[M], clo[M], chi[M], xo[M], xn[M],
+                    dummy[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    ca2[i] = s_a2[i * TC + cc]; ca1[i] = s_a1[i * TC + cc];
-                    cb2[i] = s_b2[i * TC + cc]; cb1[i] = s_b1[i * TC + cc];
-                    clo[i] = s_lo[i * TC + cc]; chi[i] = s_hi[i * TC + cc];
-                    xo[i] = s_x[i * TC + cc];
+                    const int e = i * TCM + cc;
+                    a2q[i] = s_a2q[e]; a1q[i] = s_a1q[e]; cb2[i] = s_b2[e]; cb1[i] = s_b1[e];
+                    bq[i] = s_bq[e]; ib[i] = s_ib[e]; clo[i] = s_lo[e]; chi[i] = s_hi[e];
+                    xo[i] = s_x[e];
                     dummy[i] = 0.0;
                 }
                 const double vv = s_v[cc];
                 const double yy = s_y[cc];
-                gs_cell<M, MODE>(ca2, ca1, cb2, cb1, clo, chi, xo, xn, yy, fmax(vv, 0.0),
-                                 vv < 0.0 ? -vv : 0.0, zl, rho, iq, false, dummy);
+                gs_cell_prep<M, MODE>(a2q, a1q, cb2, cb1, bq, ib, clo, chi, xo, xn, yy, fmax(vv, 0.0),
+                                      vv < 0.0 ? -vv : 0.0, zl, R, false, dummy);
                 s_v[cc] = cell_tail<M>(xo, xn, yy, vv, 1.0, is_check, my_r1, my_s3);
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    s_x[i * TC + cc] = xn[i];
-                    Sg[i] += fma(cb2[i], xn[i], cb1[i]) * xn[i];
-                    const double dg = (xn[i] - xo[i]) * fma(cb2[i], xn[i] + xo[i], cb1[i]);
-                    dgx[i] = fmax(dgx[i], dg);
-                    dgn[i] = fmin(dgn[i], dg);
+                    s_x[i * TCM + cc] = xn[i];
+                    fx[i] += __double2ll_rn(fma(cb2[i], xn[i], cb1[i]) * xn[i] * fxs[i]);
+                    if (is_check) {
+                        const double dg = (xn[i] - xo[i]) * fma(cb2[i], xn[i] + xo[i], cb1[i]);
+                        dgx[i] = fmax(dgx[i], dg);
+                        dgn[i] = fmin(dgn[i], dg);
+                    }
                 }
             }
         } else if (tile == 0) {
@@ -286,7 +352,8 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
 #pragma unroll
                     for (int i = 0; i < M; ++i) x1v[i] = __shfl_sync(0xffffffffu, c_pub, i);
                 } else {
-                    read_consensus<M>(p.pub + (size_t)((it - 1) & (PUB_BUFS - 1)) * a.m * qq, qq, qtot, x1v);
+                    read_consensus<M>(p.pub + (size_t)((it - 1) & (PUB_BUFS - 1)) * a.m * qq, qq, qtot,
+                                      x1v);
                 }
 #pragma unroll
                 for (int i = 0; i < M; ++i)
@@ -301,7 +368,8 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
             if (lane == 0)
 #pragma unroll
                 for (int i = 0; i < M; ++i)
-                    st_relaxed_u64(p.pub + ((size_t)((it + 1) & (PUB_BUFS - 1)) * a.m + i) * qq + j, PUB_EMPTY);
+                    st_relaxed_u64(p.pub + ((size_t)((it + 1) & (PUB_BUFS - 1)) * a.m + i) * qq + j,
+                                   PUB_EMPTY);
             double x1nu[M], cnu[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -309,37 +377,43 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                 x1nu[i] = __shfl_sync(0xffffffffu, c_x1, i) + cnu[i];
             }
             double xk0[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xk0[i] = 0.0;
             if (lane == 0) {
-                double ca2[M], ca1[M], cb2[M], cb1[M], clo[M], chi[M], xo[M];
+                double a2q[M], a1q[M], cb2[M], cb1[M], bq[M], ib[M], clo[M], chi[M], xo[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    ca2[i] = s_a2[i * TC]; ca1[i] = s_a1[i * TC];
-                    cb2[i] = s_b2[i * TC]; cb1[i] = s_b1[i * TC];
-                    clo[i] = s_lo[i * TC]; chi[i] = s_hi[i * TC];
-                    xo[i] = s_x[i * TC];
+                    const int e = i * TCM;
+                    a2q[i] = s_a2q[e]; a1q[i] = s_a1q[e]; cb2[i] = s_b2[e]; cb1[i] = s_b1[e];
+                    bq[i] = s_bq[e]; ib[i] = s_ib[e]; clo[i] = s_lo[e]; chi[i] = s_hi[e];
+                    xo[i] = s_x[e];
                 }
                 const double vv = s_v[0];
                 const double yy = s_y[0];
-                gs_cell<M, MODE>(ca2, ca1, cb2, cb1, clo, chi, xo, xk0, yy, fmax(vv, 0.0),
-                                 vv < 0.0 ? -vv : 0.0, zl, rho, iq, true, x1nu);
-                s_v[0] = cell_tail<M>(xo, xk0, yy, vv, 1.0, is_check, my_r1, my_s3);
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    s_x[i * TC] = xk0[i];
-                    Sg[i] += fma(cb2[i], xk0[i], cb1[i]) * xk0[i];
-                    const double dg = (xk0[i] - xo[i]) * fma(cb2[i], xk0[i] + xo[i], cb1[i]);
-                    dgx[i] = fmax(dgx[i], dg);
-                    dgn[i] = fmin(dgn[i], dg);
-                }
-                // x_1 for the check; (6c)'s contribution x_1 - nu (nu before (6h))
-#pragma unroll
-                for (int i = 0; i < M; ++i) __stcg(p.xraw + ((size_t)par * a.m + i) * qq + j, xk0[i]);
+                gs_cell_prep<M, MODE>(a2q, a1q, cb2, cb1, bq, ib, clo, chi, xo, xk0, yy, fmax(vv, 0.0),
+                                      vv < 0.0 ? -vv : 0.0, zl, R, true, x1nu);
+                // (6c)'s contribution x_1 - nu (nu before (6h)): published first
                 if (!single || is_check) {  // q = 1: only the residual check reads it
                     fence_acq_rel_gpu();
 #pragma unroll
                     for (int i = 0; i < M; ++i)
                         st_relaxed_u64(p.pub + ((size_t)(it & (PUB_BUFS - 1)) * a.m + i) * qq + j,
                                        (unsigned long long)__double_as_longlong(xk0[i] - cnu[i]));
+                }
+                s_v[0] = cell_tail<M>(xo, xk0, yy, vv, 1.0, is_check, my_r1, my_s3);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    s_x[i * TCM] = xk0[i];
+                    fx[i] += __double2ll_rn(fma(cb2[i], xk0[i], cb1[i]) * xk0[i] * fxs[i]);
+                    if (is_check) {
+                        const double dg = (xk0[i] - xo[i]) * fma(cb2[i], xk0[i] + xo[i], cb1[i]);
+                        dgx[i] = fmax(dgx[i], dg);
+                        dgn[i] = fmin(dgn[i], dg);
+                        // max/min over j of x_1 for the consensus residual
+                        unsigned long long* cs = p.chk + (size_t)(nchk % 3) * CHK_SLOTS;
+                        atomicMax(cs + 6 + i, okey(xk0[i]));
+                        atomicMin(cs + 6 + MAXM + i, okey(xk0[i]));
+                    }
                 }
             }
             // lanes i < M keep x_1 and the contribution for (6h) / the q = 1 path
@@ -352,90 +426,96 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                 }
             }
         }
-
         PHASE(0)
-        // ---- block reduction (fixed tree) of the tile partials
+        // ---- row partials: exact fixed-point warp sums, DSMEM adds into every mate
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            Sg[i] = warp_sum(Sg[i]);
-            if (is_check) {
-                dgx[i] = warp_max(dgx[i]);
-                dgn[i] = warp_min(dgn[i]);
-            }
+            const unsigned long long ws = warp_sum_u64((unsigned long long)fx[i]);
+            if (lane < T && ws != 0ull) atomicAdd(cluster.map_shared_rank(&s_acc[par][i], lane), ws);
         }
+        double cta_r1 = 0.0, cta_s3 = 0.0;
         if (is_check) {
-            my_r1 = warp_max(my_r1);
-            my_s3 = warp_max(my_s3);
-        }
-        if (lane == 0) {
+            // (checks only) tile maxima/minima of dg and CTA maxima of r1, s3: warp
+            // reductions, one CTA reduction in warp 0, DSMEM stores into every mate
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                red[wid][3 * i] = Sg[i];
-                red[wid][3 * i + 1] = dgx[i];
-                red[wid][3 * i + 2] = dgn[i];
+                const double mx = warp_max(dgx[i]), mn = warp_min(dgn[i]);
+                if (lane == 0) {
+                    s_wred[wid][i] = mx;
+                    s_wred[wid][M + i] = mn;
+                }
             }
-            red[wid][3 * M] = my_r1;
-            red[wid][3 * M + 1] = my_s3;
+            const double r1 = warp_max(my_r1), s3 = warp_max(my_s3);
+            if (lane == 0) {
+                s_wred[wid][2 * M] = r1;
+                s_wred[wid][2 * M + 1] = s3;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                double v[2 * M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    v[i] = warp_max(lane < nw ? s_wred[lane][i] : -INFINITY);
+                    v[M + i] = warp_min(lane < nw ? s_wred[lane][M + i] : INFINITY);
+                }
+                cta_r1 = warp_max(lane < nw ? s_wred[lane][2 * M] : 0.0);
+                cta_s3 = warp_max(lane < nw ? s_wred[lane][2 * M + 1] : 0.0);
+                if (lane < T) {
+                    double* dst = cluster.map_shared_rank(&s_dgp[tile][0], lane);
+#pragma unroll
+                    for (int u = 0; u < 2 * M; ++u) dst[u] = v[u];
+                }
+            }
         }
         PHASE(1)
-        __syncthreads();
-        PHASE(2)
-        double cta_r1 = 0.0, cta_s3 = 0.0;
-        if (wid == 0) {
-            double val[3 * M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                val[3 * i] = warp_sum(lane < nw ? red[lane][3 * i] : 0.0);
-                val[3 * i + 1] = is_check ? warp_max(lane < nw ? red[lane][3 * i + 1] : -INFINITY) : 0.0;
-                val[3 * i + 2] = is_check ? warp_min(lane < nw ? red[lane][3 * i + 2] : INFINITY) : 0.0;
-            }
-            if (is_check) {
-                cta_r1 = warp_max(lane < nw ? red[lane][3 * M] : 0.0);
-                cta_s3 = warp_max(lane < nw ? red[lane][3 * M + 1] : 0.0);
-            }
-            if (lane < T) {  // DSMEM: this tile's partials into mate `lane`
-                double* dst = cluster.map_shared_rank(&s_part[par][tile][0], lane);
-#pragma unroll
-                for (int v = 0; v < 3 * M; ++v) dst[v] = val[v];
-            }
-        }
-        PHASE(3)
-        cluster.sync();  // all T partials of row j are in every CTA's s_part[par]
+        cluster.sync();  // all partials of row j are in every CTA's s_acc[par] (and s_dgp)
         PHASE(4)
 
-        // ---- row update (6b),(6g),(6d),(6i): identical in every CTA of the cluster
+        // ---- row update (6b),(6g),(6d),(6i) via identity I1, identical in every CTA:
+        //   W = sum_k g - n lam, t = h + p - W, lam' = kappa t, zeta' = lam' - lam,
+        //   1'z' = W + n lam', h' = min(c, 1'z' - p), p' = p + h' - 1'z'
         if (tid < M) {
-            double sg = 0.0, mx = -INFINITY, mn = INFINITY;
-            for (int t = 0; t < T; ++t) {
-                sg += s_part[par][t][3 * tid];
-                mx = fmax(mx, s_part[par][t][3 * tid + 1]);
-                mn = fmin(mn, s_part[par][t][3 * tid + 2]);
+            const double sg = (double)(long long)s_acc[par][tid] * fxi[tid];
+            s_acc[par][tid] = 0ull;  // mates add into this buffer again after the next barrier
+            double mx = -INFINITY, mn = INFINITY;
+            if (is_check)  // s_dgp is rewritten only at the next check, 2+ barriers later
+                for (int t = 0; t < T; ++t) {
+                    mx = fmax(mx, s_dgp[t][tid]);
+                    mn = fmin(mn, s_dgp[t][M + tid]);
+                }
+            const double W = (sg + r_sb0) - nd * r_lam;
+            const double t = (r_h + r_p) - W;
+            const double lam = s_kap * t;
+            const double zeta = lam - r_lam;
+            const double oneTz = W + nd * lam;
+            const double h = fmin(r_c, oneTz - r_p);
+            const double pn = (r_p + h) - oneTz;
+            if (is_check) {
+                const double dz = zeta - r_zeta;
+                r_r2 = fabs(zeta);
+                r_r3 = fabs(h - oneTz);
+                r_s1 = fmax(mx + dz, -(mn + dz));
+                r_s2 = fabs(h - r_h);
             }
-            const RowOut o = row_update(sg, r_sb0, r_lam, r_p, r_h, r_zeta, r_c, nd, rho, mx, mn);
-            r_lam = o.lam;
-            r_zeta = o.zeta;
-            r_h = o.h;
-            r_p = o.p;
-            r_r2 = o.r2;
-            r_r3 = o.r3;
-            r_s1 = o.s1;
-            r_s2 = o.s2;
-            s_zl[tid] = r_zeta + r_lam;
+            r_lam = lam;
+            r_zeta = zeta;
+            r_h = h;
+            r_p = pn;
+            s_zl[tid] = zeta + lam;
         }
-
         PHASE(5)
+
         if (is_check) {
-            const int cpar = (int)(nchk & 1);
+            unsigned long long* cs = p.chk + (size_t)(nchk % 3) * CHK_SLOTS;
             if (tile == 0 && tid < M) {
-                double* rc = p.rowchk + (((size_t)cpar * a.m + tid) * qq + j) * 4;
-                __stcg(rc, r_r2);
-                __stcg(rc + 1, r_r3);
-                __stcg(rc + 2, r_s1);
-                __stcg(rc + 3, r_s2);
+                atomicMax(cs + 1, okey(r_r2));
+                atomicMax(cs + 2, okey(r_r3));
+                atomicMax(cs + 3, okey(r_s1));
+                atomicMax(cs + 4, okey(r_s2));
             }
             if (tid == 0) {
-                __stcg(p.rpart + ((size_t)cpar * p.G + blockIdx.x) * 2, cta_r1);
-                __stcg(p.rpart + ((size_t)cpar * p.G + blockIdx.x) * 2 + 1, cta_s3);
+                atomicMax(cs + 0, okey(cta_r1));
+                atomicMax(cs + 5, okey(cta_s3));
             }
             __syncthreads();
             ++nchk;
@@ -446,58 +526,46 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
             }
             __syncthreads();
             if (wid == 0) {
-                // x1 of this iteration (same reduction as the consensus warps) and the maxima
-                double x1v[M], xmx[M], xmn[M];
+                // x1 of this iteration (same reduction as the consensus warps)
+                double x1v[M];
                 read_consensus<M>(p.pub + (size_t)(it & (PUB_BUFS - 1)) * a.m * qq, qq, qtot, x1v);
-                const double* xr = p.xraw + (size_t)par * a.m * qq;
+                const unsigned long long kv = lane < CHK_SLOTS ? ld_relaxed_u64(cs + lane) : 0ull;
+                double v[CHK_SLOTS];
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    double mx = -INFINITY, mn = INFINITY;
-                    for (long long jj = lane; jj < qq; jj += 32) {
-                        const double x0 = __ldcg(xr + (size_t)i * qq + jj);
-                        mx = fmax(mx, x0);
-                        mn = fmin(mn, x0);
-                    }
-                    xmx[i] = warp_max(mx);
-                    xmn[i] = warp_min(mn);
-                }
-                double t0 = 0.0, t6 = 0.0, t1 = 0.0, t2 = 0.0, t4 = 0.0, t5 = 0.0;
-                for (int g = lane; g < p.G; g += 32) {
-                    t0 = fmax(t0, __ldcg(p.rpart + ((size_t)cpar * p.G + g) * 2));
-                    t6 = fmax(t6, __ldcg(p.rpart + ((size_t)cpar * p.G + g) * 2 + 1));
-                }
-                const long long R = (long long)a.m * qq;
-                for (long long r = lane; r < R; r += 32) {
-                    const double* rc = p.rowchk + ((size_t)cpar * R + r) * 4;
-                    t1 = fmax(t1, __ldcg(rc));
-                    t2 = fmax(t2, __ldcg(rc + 1));
-                    t4 = fmax(t4, __ldcg(rc + 2));
-                    t5 = fmax(t5, __ldcg(rc + 3));
-                }
-                t0 = warp_max(t0); t1 = warp_max(t1); t2 = warp_max(t2);
-                t4 = warp_max(t4); t5 = warp_max(t5); t6 = warp_max(t6);
+                for (int s = 0; s < CHK_SLOTS; ++s) v[s] = okey_inv(__shfl_sync(0xffffffffu, kv, s));
                 if (lane == 0) {
+                    // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
                     double t3 = 0.0;
                     for (int i = 0; i < M; ++i) {
-                        // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
-                        t3 = fmax(t3, fmax(xmx[i] - x1v[i], x1v[i] - xmn[i]));
+                        t3 = fmax(t3, fmax(v[6 + i] - x1v[i], x1v[i] - v[6 + MAXM + i]));
                         s_x1[i] = x1v[i];
                     }
-                    double t[7] = {t0, t1, t2, t3, t4, t5, t6};
-                    double rn[4], fl[4], r, sg, fac, s123[3];
-                    const int conv = check_decide(P, rho, t, rn, fl, &r, &sg, &fac, s123);
+                    double tt[7] = {v[0], v[1], v[2], t3, v[3], v[4], v[5]};
+                    double rho[4], rn[4], fl[4], r, sg, fac, s123[3];
+                    for (int l = 0; l < 4; ++l) rho[l] = s_rho[l];
+                    const int conv = check_decide(P, rho, tt, rn, fl, &r, &sg, &fac, s123);
                     if (blockIdx.x == 0 && a.hist && a.hist_cap > 0)
                         write_hist(a.hist + (size_t)(l_checks % a.hist_cap) * HCOLS, it + 1, r, sg,
-                                   rho, t, s123, conv, fac);
+                                   rho, tt, s123, conv, fac);
                     for (int l = 0; l < 4; ++l) {
                         s_rho[l] = rn[l];
                         s_f[l] = fl[l];
                     }
+                    s_R[0] = rn[0];
+                    s_R[1] = rn[2];
+                    s_R[2] = rn[3];
+                    s_R[3] = 1.0 / rn[0];
+                    s_kap = rn[1] / (rn[0] + nd * rn[1]);
                     s_t[0] = r;
                     s_t[1] = sg;
                     s_flag[0] = conv;
                     s_flag[1] = (!isfinite(r) || !isfinite(sg)) ? 1 : 0;
                 }
+                // CTA 0 resets the set the check after next combines into: its readers
+                // (check nchk-2) are done, its writers start after the next barrier
+                if (blockIdx.x == 0 && lane < CHK_SLOTS)
+                    st_relaxed_u64(p.chk + (size_t)((nchk + 1) % 3) * CHK_SLOTS + lane,
+                                   lane >= 6 + MAXM ? ~0ull : 0ull);
             }
             __syncthreads();
             l_r = s_t[0];
@@ -554,8 +622,8 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     }
     if (cons_warp && tile == 0 && lane < M) s_x1[lane] = c_x1;
     __syncthreads();
-    for (int t = tid; t < M * TC; t += blockDim.x) {
-        const int i = t / TC, c = t - i * TC;
+    for (int t = tid; t < M * TCM; t += blockDim.x) {
+        const int i = t / TCM, c = t - i * TCM;
         if (c < ncell) a.x[(long long)i * qn + j * a.n_pad + k0 + c] = s_x[t];
     }
     for (int c = tid; c < ncell; c += blockDim.x) a.v[j * a.n_pad + k0 + c] = s_v[c];
@@ -584,7 +652,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
         __threadfence();
         *(volatile long long*)a.iter = it;
     }
-    cluster.sync();  // no CTA exits while a mate may still write its shared memory
+    cluster.sync();  // no CTA exits while a mate may still touch its shared memory
 }
 
 }  // namespace admm_dev
