@@ -26,6 +26,7 @@
 #include "admm_kernels.cuh"
 #include "admm_persist.cuh"
 #include "admm_onchip.cuh"
+#include "admm_stream.cuh"
 
 using namespace admm_dev;
 
@@ -39,7 +40,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, total;
+        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, total;
 };
 
 int pick_bs(long long n) {
@@ -91,6 +92,9 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.ib2s = take(onchip_sized ? E : 8);
     L.chk = take(3 * CHK_SLOTS * 8);
     L.gbound = take(MAXM * 8);
+    L.rowacc = take((size_t)q * MAXM * 8);
+    L.rowdg = take((size_t)q * 2 * MAXM * 8);
+    L.rowcnt = take((size_t)q * MAXM * 4);
     L.total = o;
     return L;
 }
@@ -165,6 +169,13 @@ __global__ void gbound_kernel(int m, long long q, long long n, long long n_pad, 
             atomicMax(out + i, okey(g));
         }
     }
+}
+
+// row dg extrema accumulators of the streaming engine: identities (max 0, min ~0)
+__global__ void rowdg_init_kernel(unsigned long long* rowdg, long long q) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < q * 2 * MAXM;
+         t += (long long)gridDim.x * blockDim.x)
+        rowdg[t] = (t % (2 * MAXM)) >= MAXM ? ~0ull : 0ull;
 }
 
 // init (reading G19): x = clamp(midpoint) or clamp(0); v = s = max(0, sum_i x - y)
@@ -464,8 +475,12 @@ struct admm_ctx {
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
     bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
     int last_engine = 0;          // 1 streaming, 2 persistent grid, 3 persistent cluster
-    bool prep_ok = false;         // bq / ib2s / fixed-point scales valid for the cluster engine
+    bool prep_ok = false;         // bq / ib2s valid (on-chip-sized problems)
+    bool fx_ok = false;           // fixed-point scales of the row sums valid (finite bounds)
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
+    bool use_tma = false;         // streaming engine: TMA-pipelined sweep (else legacy sweep)
+    bool graph_dirty = true;      // problem changed since the graph was captured
+    SArgs sa{};
 };
 
 namespace {
@@ -512,6 +527,7 @@ void upload_params(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
 }
 
 typedef void (*sweep_fn)(KArgs);
+typedef void (*sweep_tma_fn)(KArgs, SArgs);
 
 sweep_fn pick_sweep(int m, int mode) {
 #define S(MM)                                                                                  \
@@ -521,11 +537,76 @@ sweep_fn pick_sweep(int m, int mode) {
     return nullptr;
 }
 
+sweep_tma_fn pick_sweep_tma(int m, int mode, int* tl, size_t* smem) {
+#define S(MM)                                                                                  \
+    if (m == MM) {                                                                             \
+        *tl = StreamCfg<MM>::TL;                                                               \
+        *smem = StreamCfg<MM>::SMEM;                                                           \
+        return mode == BOX_EXACT ? sweep_tma_kernel<MM, BOX_EXACT> : sweep_tma_kernel<MM, BOX_PROJECT>; \
+    }
+    S(1) S(2) S(3) S(4)
+#undef S
+    return nullptr;
+}
+
+// streaming engine configuration: TMA sweep when the fixed-point scales exist
+admm_status plan_stream(admm_ctx* ctx) {
+    int tl = 0;
+    size_t smem = 0;
+    sweep_tma_fn tf = pick_sweep_tma(ctx->m, ctx->params.box_mode, &tl, &smem);
+    // The TMA-pipelined sweep (admm_stream.cuh) is opt-in: on B200 the register-
+    // bound 2-cells-per-thread sweep_kernel measured faster (44-47 % vs 37 % of
+    // HBM peak at q = 1e4..1e5, profiles/README.md), the fp64 chain latency and
+    // not the load/compute overlap being the limiter.
+    const char* opt = getenv("ADMM_STREAM_TMA");
+    ctx->use_tma = tf && ctx->fx_ok && (opt && opt[0] == '1');
+    if (!ctx->use_tma) return ADMM_OK;
+    if (cudaFuncSetAttribute((const void*)tf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        ctx->use_tma = false;
+        return ADMM_OK;
+    }
+    if (const char* dbg = getenv("ADMM_DEBUG")) {
+        if (dbg[0] == '1') {
+            cudaFuncAttributes fa;
+            if (cudaFuncGetAttributes(&fa, (const void*)tf) == cudaSuccess)
+                fprintf(stderr, "[admm] sweep_tma: regs %d maxThreads %d static smem %zu dyn max %d local %zu\n",
+                        fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+                        fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+        }
+    }
+    SArgs& sa = ctx->sa;
+    sa.TL = tl;
+    sa.TPR = (int)((ctx->n + tl - 1) / tl);
+    sa.G = ctx->sms;
+    // rows are split into S segments only when there are too few rows to balance the SMs
+    const long long q = ctx->q;
+    sa.S = q >= 8LL * sa.G ? 1 : (int)std::min<long long>(sa.TPR, (8LL * sa.G + q - 1) / q);
+    sa.TPS = (sa.TPR + sa.S - 1) / sa.S;
+    sa.S = (sa.TPR + sa.TPS - 1) / sa.TPS;
+    sa.U = (int)(q * sa.S);
+    for (int i = 0; i < MAXM; ++i) {
+        sa.fx_scale[i] = ctx->fx_scale[i];
+        sa.fx_inv[i] = ctx->fx_inv[i];
+    }
+    sa.rowacc = (unsigned long long*)(ctx->ws + ctx->L.rowacc);
+    sa.rowdg = (unsigned long long*)(ctx->ws + ctx->L.rowdg);
+    sa.rowcnt = (unsigned*)(ctx->ws + ctx->L.rowcnt);
+    return ADMM_OK;
+}
+
 // body of one while-loop pass: check_every iterations
 admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
     const int K = std::max(1, ctx->params.check_every);
+    int tl = 0;
+    size_t smem = 0;
+    sweep_tma_fn tf = pick_sweep_tma(ctx->m, ctx->params.box_mode, &tl, &smem);
     for (int r = 0; r < K; ++r) {
-        fn<<<ctx->G, ctx->bs, 0, st>>>(ctx->ka);
+        if (ctx->use_tma)
+            tf<<<ctx->sa.G, ctx->sa.TL, smem, st>>>(ctx->ka, ctx->sa);
+        else
+            fn<<<ctx->G, ctx->bs, 0, st>>>(ctx->ka);
         CKC(cudaGetLastError());
         if (ctx->world > 1) {
             CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, st));
@@ -544,7 +625,7 @@ __global__ void set_cond_kernel(KArgs a, cudaGraphConditionalHandle h) {
 }
 
 admm_status build_graph(admm_ctx* ctx) {
-    if (ctx->gexec && ctx->graph_mode == ctx->params.box_mode) return ADMM_OK;
+    if (ctx->gexec && ctx->graph_mode == ctx->params.box_mode && !ctx->graph_dirty) return ADMM_OK;
     if (ctx->gexec) {
         cudaGraphExecDestroy(ctx->gexec);
         ctx->gexec = nullptr;
@@ -561,6 +642,10 @@ admm_status build_graph(admm_ctx* ctx) {
     const long long items = ctx->q * ctx->T;
     ctx->G = (int)std::max(1LL, std::min(items, (long long)occ * ctx->sms));
     ctx->ka.G = ctx->G;
+    {
+        admm_status ps = plan_stream(ctx);
+        if (ps != ADMM_OK) return ps;
+    }
     if (ctx->world == 1) {
         CKC(cudaGraphCreate(&ctx->graph, 0));
         cudaGraphConditionalHandle h;
@@ -591,6 +676,7 @@ admm_status build_graph(admm_ctx* ctx) {
     }
     CKC(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
     ctx->graph_mode = ctx->params.box_mode;
+    ctx->graph_dirty = false;
     return ADMM_OK;
 }
 
@@ -698,7 +784,7 @@ cluster_fn pick_cluster(int m, int mode) {
 // long row does not fit the shared memory of T CTAs).
 PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     PPlan pl;
-    if (ctx->world > 1 || !fn || !ctx->prep_ok) return pl;
+    if (ctx->world > 1 || !fn || !ctx->prep_ok || !ctx->fx_ok) return pl;
     const long long n = ctx->n, q = ctx->q;
     const int sms = ctx->sms;
     if (q > 32LL * sms) return pl;
@@ -1132,17 +1218,18 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
         }
         return fail(ctx, (kind == 2 || kind == 3) ? ADMM_ERR_NONCONVEX : ADMM_ERR_INVALID, buf);
     }
-    // on-chip engine: prepared constants and the fixed-point scales of the row sums
+    // fixed-point scales of the row sums (every engine), prepared constants (on-chip engine)
     ctx->prep_ok = false;
-    if ((size_t)ctx->m * ctx->q * ctx->n_pad <= ONCHIP_PREP_MAX_ELEMS) {
-        const long long NE = (long long)ctx->m * ctx->q * ctx->n_pad;
-        prep_kernel<<<grid_for(NE, 256, ctx->sms), 256, 0, ctx->stream>>>(
-            NE, a.b2, a.b1, (double*)(ctx->ws + ctx->L.bq), (double*)(ctx->ws + ctx->L.ib2s));
-        CKC(cudaGetLastError());
+    ctx->fx_ok = false;
+    ctx->graph_dirty = true;
+    {
         unsigned long long* gb = (unsigned long long*)(ctx->ws + ctx->L.gbound);
         CKC(cudaMemsetAsync(gb, 0, MAXM * 8, ctx->stream));
         gbound_kernel<<<grid_for(blk, 256, ctx->sms), 256, 0, ctx->stream>>>(
             ctx->m, ctx->q, ctx->n, ctx->n_pad, a.b2, a.b1, a.lo, a.hi, gb);
+        CKC(cudaGetLastError());
+        rowdg_init_kernel<<<grid_for(ctx->q * 2 * MAXM, 256, ctx->sms), 256, 0, ctx->stream>>>(
+            (unsigned long long*)(ctx->ws + ctx->L.rowdg), ctx->q);
         CKC(cudaGetLastError());
         unsigned long long keys[MAXM];
         CKC(cudaMemcpyAsync(keys, gb, MAXM * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1164,7 +1251,14 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             ctx->fx_scale[i] = std::ldexp(1.0, E);
             ctx->fx_inv[i] = std::ldexp(1.0, -E);
         }
-        ctx->prep_ok = ok;
+        ctx->fx_ok = ok;
+    }
+    if (ctx->fx_ok && (size_t)ctx->m * ctx->q * ctx->n_pad <= ONCHIP_PREP_MAX_ELEMS) {
+        const long long NE = (long long)ctx->m * ctx->q * ctx->n_pad;
+        prep_kernel<<<grid_for(NE, 256, ctx->sms), 256, 0, ctx->stream>>>(
+            NE, a.b2, a.b1, (double*)(ctx->ws + ctx->L.bq), (double*)(ctx->ws + ctx->L.ib2s));
+        CKC(cudaGetLastError());
+        ctx->prep_ok = true;
     }
     admm_status is = init_state(ctx);
     if (is != ADMM_OK) return is;

@@ -499,9 +499,11 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
                 if (valid) {
                     const double b2 = cb2[i][c], b1 = cb1[i][c];
                     Sg[i] += fma(b2, xn[i][c], b1) * xn[i][c];
-                    const double dg = (xn[i][c] - xo[i][c]) * fma(b2, xn[i][c] + xo[i][c], b1);
-                    dgx[i] = fmax(dgx[i], dg);
-                    dgn[i] = fmin(dgn[i], dg);
+                    if (is_check) {  // sigma's z-term only
+                        const double dg = (xn[i][c] - xo[i][c]) * fma(b2, xn[i][c] + xo[i][c], b1);
+                        dgx[i] = fmax(dgx[i], dg);
+                        dgn[i] = fmin(dgn[i], dg);
+                    }
                 }
             }
         }
