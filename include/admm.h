@@ -75,9 +75,19 @@ typedef enum {
 typedef enum {
     ADMM_EXEC_AUTO = 0,       /* persistent when the state fits on chip, else streaming */
     ADMM_EXEC_STREAMING = 1,  /* one fused sweep kernel per iteration, CUDA-graph while loop */
-    ADMM_EXEC_PERSISTENT = 2  /* one cooperative kernel per call, state in shared memory;
-                                 ADMM_ERR_INVALID if the problem does not fit on chip */
+    ADMM_EXEC_PERSISTENT = 2  /* one kernel per call, state in shared memory (cluster-row
+                                 engine, else grid-barrier engine); ADMM_ERR_INVALID if the
+                                 problem does not fit on chip */
 } admm_exec_mode;
+
+/* Engine that ran the last admm_iterate / admm_solve (admm_get_engine). */
+typedef enum {
+    ADMM_ENGINE_NONE = 0,
+    ADMM_ENGINE_STREAM = 1,      /* sweep_kernel: one launch per iteration (graph while loop) */
+    ADMM_ENGINE_GRID = 2,        /* persist_kernel: one cooperative launch per call */
+    ADMM_ENGINE_CLUSTER = 3,     /* persist_cluster_kernel: one cluster launch per call */
+    ADMM_ENGINE_STREAM_TMA = 4   /* sweep_tma_kernel (opt-in: env ADMM_STREAM_TMA=1) */
+} admm_engine;
 
 /* Scenario sharding across ranks (one process per GPU).  Rank r owns the
    scenarios j in [j_begin, j_end) of q_total.  nccl_id comes from
@@ -189,6 +199,12 @@ int64_t admm_get_history(admm_ctx* ctx, double* out, int64_t max_rows);
 /* Average device time (ms) of each kernel class over the last solve/iterate
    call, measured with CUDA events; out[0] = sweep kernel, out[1] = whole call. */
 admm_status admm_get_timing(admm_ctx* ctx, double out[2]);
+
+/* Engine of the last iterate/solve call (admm_engine) and the number of CUDA
+   kernels this context has launched since admm_create (cumulative; resets,
+   sweeps, graph condition kernels, objective).  Either pointer may be NULL.
+   ADMM_ERR_INVALID on a NULL context. */
+admm_status admm_get_engine(const admm_ctx* ctx, int32_t* engine, int64_t* launches);
 
 const char* admm_last_error(const admm_ctx* ctx);
 void admm_destroy(admm_ctx* ctx);

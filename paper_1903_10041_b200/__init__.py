@@ -18,6 +18,7 @@ from ._lib import (  # noqa: F401
     admm_create,
     admm_default_params,
     admm_destroy,
+    admm_get_engine,
     admm_get_history,
     admm_get_params,
     admm_get_solution,

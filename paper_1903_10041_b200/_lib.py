@@ -75,6 +75,7 @@ _sigs = {
     "admm_set_state": (C.c_int, [_ctx_p] + [_vp] * 9 + [C.c_int32]),
     "admm_get_history": (C.c_int64, [_ctx_p, _vp, C.c_int64]),
     "admm_get_timing": (C.c_int, [_ctx_p, C.c_double * 2]),
+    "admm_get_engine": (C.c_int, [_ctx_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "admm_last_error": (C.c_char_p, [_ctx_p]),
     "admm_destroy": (None, [_ctx_p]),
     "quartic_minimize_batch": (C.c_int, [_vp] * 7 + [C.c_int64, C.c_int32, _vp]),
@@ -220,6 +221,17 @@ def admm_get_timing(ctx):
     t = (C.c_double * 2)()
     _check(ctx, _lib.admm_get_timing(ctx, t))
     return t[0], t[1]
+
+
+ENGINE_NAMES = {0: "none", 1: "sweep_kernel", 2: "persist_kernel", 3: "persist_cluster_kernel",
+                4: "sweep_tma_kernel"}
+
+
+def admm_get_engine(ctx):
+    """(engine id of the last call, kernels launched by this context so far)."""
+    e, n = C.c_int32(0), C.c_int64(0)
+    _check(ctx, _lib.admm_get_engine(ctx, C.byref(e), C.byref(n)))
+    return int(e.value), int(n.value)
 
 
 def admm_last_error(ctx) -> str:

@@ -474,7 +474,8 @@ struct admm_ctx {
     long long* h_iter = nullptr;  // pinned
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
     bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
-    int last_engine = 0;          // 1 streaming, 2 persistent grid, 3 persistent cluster
+    int last_engine = 0;          // ADMM_ENGINE_* of the last iterate/solve
+    long long launches = 0;       // kernels launched by this context since create
     bool prep_ok = false;         // bq / ib2s valid (on-chip-sized problems)
     bool fx_ok = false;           // fixed-point scales of the row sums valid (finite bounds)
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
@@ -762,6 +763,7 @@ admm_status launch_persist(admm_ctx* ctx, persist_fn fn, const PPlan& pl) {
     KArgs ka = ctx->ka;
     void* args[] = {&ka, &pa};
     CKC(cudaLaunchCooperativeKernel((const void*)fn, pl.G, pl.BS, args, pl.smem, ctx->stream));
+    ctx->launches += 1;
     return ADMM_OK;
 }
 
@@ -882,6 +884,7 @@ admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     CKC(cudaLaunchKernelEx(&cfg, fn, ctx->ka, ca));
+    ctx->launches += 2;  // onchip_reset_kernel + the cluster kernel
     return ADMM_OK;
 }
 
@@ -909,10 +912,14 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         st = build_graph(ctx);
         if (st != ADMM_OK) return st;
     }
-    ctx->last_engine = cpl.ok ? 3 : (pl.ok ? 2 : 1);
+    ctx->last_engine = cpl.ok ? ADMM_ENGINE_CLUSTER
+                              : (pl.ok ? ADMM_ENGINE_GRID
+                                       : (ctx->use_tma ? ADMM_ENGINE_STREAM_TMA : ADMM_ENGINE_STREAM));
     upload_params(ctx, iter_limit, stop_on_conv);
     clear_done_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ka);
+    ctx->launches += 1;
     const long long start = ctx->iter_host;
+    long long graph_bodies = 0;
     CKC(cudaEventRecord(ctx->e0, ctx->stream));
     if (cpl.ok) {
         st = launch_cluster(ctx, cfn, cpl);
@@ -926,16 +933,19 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
+            ctx->launches += (long long)std::max(1, ctx->params.check_every) * (ctx->world > 1 ? 2 : 1);
             st = read_ctrl(ctx);
             if (st != ADMM_OK) return st;
             if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
         }
     } else if (ctx->world == 1) {
         CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
+        graph_bodies = -1;  // counted after the call from the iterations done
     } else {
         const int K = std::max(1, ctx->params.check_every);
         while (true) {
             CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
+            ++graph_bodies;
             st = read_ctrl(ctx);
             if (st != ADMM_OK) return st;
             if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
@@ -950,6 +960,11 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     ctx->t_call_ms = ms;
     const long long did = ctx->iter_host - start;
     ctx->t_sweep_ms = did > 0 ? ms / (double)did : 0.0;
+    {
+        const long long K = std::max(1, ctx->params.check_every);
+        if (graph_bodies < 0) graph_bodies = std::max(1LL, (did + K - 1) / K);  // while-node passes
+        ctx->launches += graph_bodies * (K * (ctx->world > 1 ? 2 : 1) + (ctx->world > 1 ? 0 : 1));
+    }
     if (ctx->h_ctrl->err) return fail(ctx, ADMM_ERR_NUMERICAL, "NaN/Inf in residuals");
     return ADMM_OK;
 }
@@ -968,6 +983,7 @@ admm_status compute_objective(admm_ctx* ctx, double* out) {
     const long long R = (long long)ctx->m * ctx->q;
     obj_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(ctx->ka, ctx->obj_rows);
     obj_sum_kernel<<<1, 32, 0, ctx->stream>>>(R, ctx->obj_rows, ctx->ka.xsend);
+    ctx->launches += 2;
     CKC(cudaGetLastError());
     double tot = 0.0;
     if (ctx->world > 1) {
@@ -1018,6 +1034,7 @@ admm_status init_state(admm_ctx* ctx) {
         CKN(ncclAllGather(a.xsend, a.xall, XB, ncclDouble, ctx->comm, ctx->stream));
         agg = a.xall;
     }
+    ctx->launches += 4;  // init_cells, init_rows, cons_partial, init_ctrl
     init_ctrl_kernel<<<1, 32, 0, ctx->stream>>>(a, agg, ctx->world, ctx->params.rho[0],
                                                  ctx->params.rho[1], ctx->params.rho[2],
                                                  ctx->params.rho[3]);
@@ -1445,6 +1462,13 @@ int64_t admm_get_history(admm_ctx* ctx, double* out, int64_t max_rows) {
         memcpy(out + r * HCOLS, all.data() + idx * HCOLS, HCOLS * 8);
     }
     return take;
+}
+
+admm_status admm_get_engine(const admm_ctx* ctx, int32_t* engine, int64_t* launches) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (engine) *engine = ctx->last_engine;
+    if (launches) *launches = ctx->launches;
+    return ADMM_OK;
 }
 
 admm_status admm_get_timing(admm_ctx* ctx, double out[2]) {

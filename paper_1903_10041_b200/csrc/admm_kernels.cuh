@@ -585,14 +585,30 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             __syncthreads();
             if (s_last) {
                 __threadfence();
-                if (tid < M) {
-                    const double* rp = a.row_part + ((long long)tid * a.q + j) * a.T * 3;
-                    double Sgs = 0.0, mx = -INFINITY, mn = INFINITY;
-                    for (int t = 0; t < a.T; ++t) {
-                        Sgs += __ldcg(rp + 3 * t);
-                        mx = fmax(mx, __ldcg(rp + 3 * t + 1));
-                        mn = fmin(mn, __ldcg(rp + 3 * t + 2));
+                // tile partials of row j: lane-strided loads (all in flight), fixed-order
+                // per-lane sums and a butterfly (deterministic); lane i keeps source i
+                double Sgs = 0.0, mx = -INFINITY, mn = INFINITY;
+                if (wid == 0) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        const double* rp = a.row_part + ((long long)i * a.q + j) * a.T * 3;
+                        double ls = 0.0, lx = -INFINITY, ln = INFINITY;
+                        for (int t = lane; t < a.T; t += 32) {
+                            ls += __ldcg(rp + 3 * t);
+                            lx = fmax(lx, __ldcg(rp + 3 * t + 1));
+                            ln = fmin(ln, __ldcg(rp + 3 * t + 2));
+                        }
+                        ls = warp_sum(ls);
+                        lx = warp_max(lx);
+                        ln = warp_min(ln);
+                        if (lane == i) {
+                            Sgs = ls;
+                            mx = lx;
+                            mn = ln;
+                        }
                     }
+                }
+                if (tid < M) {
                     double r2, r3, s1, s2;
                     finalize_row(a, cin, tid, j, Sgs, mx, mn, &r2, &r3, &s1, &s2);
                     my_r2 = fmax(my_r2, r2);

@@ -131,6 +131,10 @@ class AdmmSolver:
         """(average device ms per iteration, device ms of the last call)."""
         return _lib.admm_get_timing(self.ctx)
 
+    def engine(self):
+        """(engine id of the last iterate/solve, kernels launched so far)."""
+        return _lib.admm_get_engine(self.ctx)
+
     def close(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:
             _lib.admm_destroy(self.ctx)
