@@ -43,10 +43,14 @@ struct Layout {
         prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, total;
 };
 
+// streaming sweep block size: 2 cells per thread, at most ADMM_SWEEP_BS (default
+// 512: one row per item; 256 splits rows over two CTAs and measured 30 % vs 44 %)
 int pick_bs(long long n) {
+    long long cap = 512;
+    if (const char* e = getenv("ADMM_SWEEP_BS")) cap = std::max(32LL, std::min(512LL, atoll(e)));
     long long need = (n + CPT - 1) / CPT;
     long long bs = ((need + 31) / 32) * 32;
-    return (int)std::max(32LL, std::min(512LL, bs));
+    return (int)std::max(32LL, std::min(cap, bs));
 }
 
 constexpr size_t ONCHIP_PREP_MAX_ELEMS = (size_t)1 << 23;  // m*q*n_pad of the largest on-chip problem
@@ -530,9 +534,24 @@ void upload_params(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
 typedef void (*sweep_fn)(KArgs);
 typedef void (*sweep_tma_fn)(KArgs, SArgs);
 
-sweep_fn pick_sweep(int m, int mode) {
+// Barrier-free (fixed-point, last-warp-finalises) sweep for rows spanning several
+// tiles (horizon n = 1e6: 26 -> 34 % of HBM peak); the barrier variant stays for
+// one-tile rows, where it measured faster (44 vs 38 % at q = 1e4, profiles/README.md).
+bool use_fx_sweep(const admm_ctx* ctx) {
+    const char* e = getenv("ADMM_SWEEP_FX");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return ctx->fx_ok;
+    return ctx->fx_ok && ctx->T > 1;
+}
+
+sweep_fn pick_sweep(int m, int mode, bool fx) {
 #define S(MM)                                                                                  \
-    if (m == MM) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT> : sweep_kernel<MM, BOX_PROJECT>;
+    if (m == MM) {                                                                             \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true>                   \
+                                         : sweep_kernel<MM, BOX_PROJECT, true>;                \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false>                          \
+                                 : sweep_kernel<MM, BOX_PROJECT, false>;                       \
+    }
     S(1) S(2) S(3) S(4)
 #undef S
     return nullptr;
@@ -635,7 +654,7 @@ admm_status build_graph(admm_ctx* ctx) {
         cudaGraphDestroy(ctx->graph);
         ctx->graph = nullptr;
     }
-    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode);
+    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx));
     if (!fn) return fail(ctx, ADMM_ERR_INVALID, "m must be in 1..4");
     int occ = 0;
     CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, 0));
@@ -929,7 +948,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         if (st != ADMM_OK) return st;
     } else if (ctx->no_graph) {
         // profiling mode (ADMM_NO_GRAPH=1): plain launches, host polls per body
-        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode);
+        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx));
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
@@ -1175,6 +1194,9 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     a.ctrl = (Ctrl*)(w + L.ctrl); a.iter = (long long*)(w + L.iter);
     a.prm = (const DParams*)(w + L.prm);
     a.hist = (double*)(w + L.hist); a.hist_cap = HIST_CAP;
+    a.rowacc = (unsigned long long*)(w + L.rowacc);
+    a.rowdg = (unsigned long long*)(w + L.rowdg);
+    a.rowcnt = (unsigned*)(w + L.rowcnt);
     ctx->vflag = (unsigned long long*)(w + L.vflag);
     ctx->obj_rows = (double*)(w + L.obj_rows);
     if (ctx->world > 1) {
@@ -1269,6 +1291,10 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             ctx->fx_inv[i] = std::ldexp(1.0, -E);
         }
         ctx->fx_ok = ok;
+        for (int i = 0; i < MAXM; ++i) {
+            ctx->ka.fx_scale[i] = ok ? ctx->fx_scale[i] : 0.0;
+            ctx->ka.fx_inv[i] = ok ? ctx->fx_inv[i] : 0.0;
+        }
     }
     if (ctx->fx_ok && (size_t)ctx->m * ctx->q * ctx->n_pad <= ONCHIP_PREP_MAX_ELEMS) {
         const long long NE = (long long)ctx->m * ctx->q * ctx->n_pad;

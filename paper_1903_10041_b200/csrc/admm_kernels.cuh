@@ -75,7 +75,32 @@ struct KArgs {
     const DParams *prm;
     double *hist;
     int hist_cap;
+    // fixed-point row sums (streaming sweep, FX variant): scale 2^E_i, accumulators for
+    // rows split over tiles (kept zero between uses), see admm_onchip.cuh / DESIGN.md §5
+    double fx_scale[MAXM], fx_inv[MAXM];
+    unsigned long long *rowacc;  // [q][MAXM]
+    unsigned long long *rowdg;   // [q][2 MAXM] ordered keys (checks)
+    unsigned *rowcnt;            // [q][MAXM]
 };
+
+// order-preserving map double -> uint64 (max/min of keys = max/min of values)
+__device__ __forceinline__ unsigned long long okey(double x) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+    const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double((long long)u);
+}
+
+// exact warp sum of 64-bit two's-complement values (mod 2^64): three 21/21/22-bit
+// limbs, each summed by redux.sync (no carries lost: 32 * 2^22 < 2^32)
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+    const unsigned l0 = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0x1FFFFFull));
+    const unsigned l1 = __reduce_add_sync(0xffffffffu, (unsigned)((v >> 21) & 0x1FFFFFull));
+    const unsigned l2 = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 42));
+    return (unsigned long long)l0 + ((unsigned long long)l1 << 21) + ((unsigned long long)l2 << 42);
+}
 
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
@@ -130,6 +155,60 @@ __device__ __forceinline__ void gs_cell(const double* ca2, const double* ca1, co
                                        clo[i], chi[i]);
         } else {
             xn[i] = clampd(-D * rcp_nr(2.0 * C), clo[i], chi[i]);  // A = B = 0: quadratic
+        }
+    }
+}
+
+// (6a) for two cells of the same thread with interleaved Gauss-Seidel chains:
+// source i of both cells is built, then minimised together (quartic_core2:
+// straight-line trig evaluations that the scheduler interleaves), so the two
+// dependency chains overlap (ILP 2).  Same arithmetic as two gs_cell calls.
+// Arrays are [M][2] (cell index last); k0 marks cell 0 as the consensus cell.
+template <int M, int MODE>
+__device__ __forceinline__ void gs_cell2(const double (*ca2)[2], const double (*ca1)[2],
+                                         const double (*cb2)[2], const double (*cb1)[2],
+                                         const double (*clo)[2], const double (*chi)[2],
+                                         const double (*xo)[2], double (*xn)[2], const double* y,
+                                         const double* s_e, const double* mu_e, const double* zl,
+                                         const double* rho, double iq, bool k0, const double* x1nu) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double C[2], D[2], bn[2], cn[2], dn[2], lo[2], hi[2];
+        bool quart[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            double others = 0.0;
+#pragma unroll
+            for (int l = 0; l < M; ++l)
+                if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
+            const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
+            const double xoi = xo[i][u];
+            const double b2 = cb2[i][u], b1 = cb1[i][u];
+            const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
+            C[u] = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i][u], iq, 0.5 * rho[2]));
+            D[u] = fma(-rho[0] * b1, e, fma(ca1[i][u], iq, -rho[2] * phi));
+            if (k0 && u == 0) {
+                C[u] += 0.5 * rho[3];
+                D[u] += -rho[3] * x1nu[i];
+            }
+            quart[u] = (b2 != 0.0);
+            const double ia2 = rcp_nr(quart[u] ? rho[0] * b2 * b2 : 1.0);  // 1 / 2A
+            bn[u] = 1.5 * (rho[0] * b2 * b1) * ia2;
+            cn[u] = C[u] * ia2;
+            dn[u] = 0.5 * D[u] * ia2;
+            lo[u] = clo[i][u];
+            hi[u] = chi[i][u];
+        }
+        if (quart[0] && quart[1]) {
+            double r[2];
+            quartic_core2<MODE>(bn, cn, dn, C, D, lo, hi, r);
+            xn[i][0] = r[0];
+            xn[i][1] = r[1];
+        } else {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                xn[i][u] = quart[u] ? quartic_core<MODE>(bn[u], cn[u], dn[u], C[u], D[u], lo[u], hi[u])
+                                    : clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
         }
     }
 }
@@ -361,7 +440,11 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
     *s2 = o.s2;
 }
 
-template <int M, int MODE>
+// FX = true (every problem with a finite box): row sums in exact fixed point,
+// per-warp slots and a last-warp finaliser -- no block barrier inside the item
+// loop, so one warp's loads overlap another warp's fp64 work.  FX = false
+// (an infinite bound): fp64 block reductions with barriers.
+template <int M, int MODE, bool FX>
 __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
     const long long it = *(volatile long long*)a.iter;
     const Ctrl& cin = a.ctrl[it & 1];
@@ -369,13 +452,21 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
     const int ce = a.prm->check_every;
     const bool is_check = ce > 0 && ((it + 1) % ce) == 0;
 
-    __shared__ double red[16][3 * M + 2];
+    __shared__ double red[16][(3 * M + 2) > 6 ? (3 * M + 2) : 6];
     __shared__ double rowres[3 * M];
     __shared__ double k0x[M], k0nu[M];
     __shared__ double acc[XB];
     __shared__ int s_last;
+    constexpr int UB = 4;                            // item slots in flight (FX)
+    __shared__ unsigned long long s_fxw[UB][16][M];  // per-warp fixed-point row partials
+    __shared__ double s_dgw[UB][16][2 * M];          // per-warp dg extrema (checks)
+    __shared__ unsigned s_arr[UB], s_gen[UB];        // arrivals, finalisations per slot
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    if (FX && tid < UB) {
+        s_arr[tid] = 0u;
+        s_gen[tid] = 0u;
+    }
     if (tid < XB) {
         double init = 0.0;
         if (tid >= MAXM && tid < MAXM + M) init = -INFINITY;      // x0max
@@ -397,9 +488,32 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
     // row-level check maxima, held by thread i < M for source i
     double my_r2 = 0.0, my_r3 = 0.0, my_s1 = 0.0, my_s2 = 0.0;
 
-    for (long long item = blockIdx.x; item < nitems; item += a.G) {
+    if (FX) __syncthreads();  // slot counters initialised
+    long long litem = 0;
+    for (long long item = blockIdx.x; item < nitems; item += a.G, ++litem) {
         const long long j = item / a.T;
         const int tile = (int)(item - j * a.T);
+        {
+            // L2 prefetch of the next item's streams (one bulk prefetch per stream row),
+            // so its loads hit L2 instead of exposing HBM latency at the item start
+            const long long nx = item + a.G;
+            if (nx < nitems && tid < 5 * M + 2) {
+                const long long jn = nx / a.T;
+                const int kn = (int)(nx - jn * a.T) * a.tile;
+                const int nc = min(a.tile, a.n_pad - kn);
+                const unsigned bytes = (unsigned)(nc * 8) & ~15u;
+                const double* src;
+                if (tid < 5 * M) {
+                    const int i = tid / 5, s5 = tid - 5 * (tid / 5);
+                    const double* base = s5 == 0 ? a.x : s5 == 1 ? a.a2 : s5 == 2 ? a.a1 : s5 == 3 ? a.b2 : a.b1;
+                    src = base + (long long)i * qn + jn * a.n_pad + kn;
+                } else {
+                    src = (tid == 5 * M ? a.y : a.v) + jn * a.n_pad + kn;
+                }
+                if (bytes)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+            }
+        }
         const int k = tile * a.tile + CPT * tid;  // first of this thread's 2 cells
         const bool inb = k < a.n_pad;             // n_pad % 4 == 0: both cells in bounds
         const bool v0 = k < a.n, v1 = (k + 1) < a.n;
@@ -466,26 +580,26 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             x1nu[i] = cin.x1[i] + nu_e[i];
         }
         double vn[2];
+        {
+            const double s_e[2] = {fmax(vv[0], 0.0), fmax(vv[1], 0.0)};
+            const double mu_e[2] = {vv[0] < 0.0 ? -vv[0] * f[2] : 0.0, vv[1] < 0.0 ? -vv[1] * f[2] : 0.0};
+            gs_cell2<M, MODE>(ca2, ca1, cb2, cb1, clo, chi, xo, xn, yv, s_e, mu_e, zl, rho, iq,
+                              owns_k0, x1nu);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            double tca2[M], tca1[M], tcb2[M], tcb1[M], tlo[M], thi[M], txo[M], txn[M];
+            for (int c = 0; c < 2; ++c) {
+                double txo[M], txn[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                tca2[i] = ca2[i][c]; tca1[i] = ca1[i][c]; tcb2[i] = cb2[i][c]; tcb1[i] = cb1[i][c];
-                tlo[i] = clo[i][c]; thi[i] = chi[i][c]; txo[i] = xo[i][c];
+                for (int i = 0; i < M; ++i) {
+                    txo[i] = xo[i][c];
+                    txn[i] = xn[i][c];
+                }
+                const bool valid = c == 0 ? v0 : v1;
+                double r1l = my_r1, s3l = my_s3;
+                const double vnew = cell_tail<M>(txo, txn, yv[c], vv[c], f[2], is_check && valid, r1l, s3l);
+                my_r1 = r1l;
+                my_s3 = s3l;
+                vn[c] = valid ? vnew : 0.0;
             }
-            const double s_e = fmax(vv[c], 0.0);
-            const double mu_e = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
-            gs_cell<M, MODE>(tca2, tca1, tcb2, tcb1, tlo, thi, txo, txn, yv[c], s_e, mu_e, zl, rho,
-                             iq, owns_k0 && c == 0, x1nu);
-            const bool valid = c == 0 ? v0 : v1;
-            double r1l = my_r1, s3l = my_s3;
-            const double vnew = cell_tail<M>(txo, txn, yv[c], vv[c], f[2], is_check && valid, r1l, s3l);
-            my_r1 = r1l;
-            my_s3 = s3l;
-            vn[c] = valid ? vnew : 0.0;
-#pragma unroll
-            for (int i = 0; i < M; ++i) xn[i][c] = txn[i];
         }
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -523,6 +637,97 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             }
         }
 
+        if constexpr (FX) {
+            // ---- (6c) consensus contribution of k = 0 (thread 0 of warp 0: item order)
+            if (owns_k0 && tile == 0) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    acc[i] += xn[i][0] - nu_e[i];
+                    acc[MAXM + i] = fmax(acc[MAXM + i], xn[i][0]);
+                    acc[2 * MAXM + i] = fmin(acc[2 * MAXM + i], xn[i][0]);
+                }
+            }
+            // ---- row partials: exact fixed point into this warp's slot of item litem
+            const int b = (int)(litem & (UB - 1));
+            if (lane == 0)  // slot b free: the finaliser of item litem - UB is done with it
+                while (*(volatile unsigned*)&s_gen[b] != (unsigned)(litem >> 2)) {
+                }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                long long fx = 0;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if (c == 0 ? v0 : v1)
+                        fx += __double2ll_rn(fma(cb2[i][c], xn[i][c], cb1[i][c]) * xn[i][c] * a.fx_scale[i]);
+                const unsigned long long ws = warp_sum_u64((unsigned long long)fx);
+                if (lane == 0) s_fxw[b][wid][i] = ws;
+                if (is_check) {
+                    const double mx = warp_max(dgx[i]), mn = warp_min(dgn[i]);
+                    if (lane == 0) {
+                        s_dgw[b][wid][i] = mx;
+                        s_dgw[b][wid][M + i] = mn;
+                    }
+                }
+            }
+            unsigned last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = (atomicAdd(&s_arr[b], 1u) == (unsigned)nw - 1);
+                __threadfence_block();
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                // ---- this warp arrived last: row finalisation (6b),(6g),(6d),(6i)
+                if (lane < M) {
+                    const int i = lane;
+                    unsigned long long part = 0ull;
+                    double mx = -INFINITY, mn = INFINITY;
+                    for (int w = 0; w < nw; ++w) {
+                        part += s_fxw[b][w][i];
+                        if (is_check) {
+                            mx = fmax(mx, s_dgw[b][w][i]);
+                            mn = fmin(mn, s_dgw[b][w][M + i]);
+                        }
+                    }
+                    bool fin = true;
+                    if (a.T > 1) {  // row split over tiles: global exact sums, last tile finalises
+                        atomicAdd(a.rowacc + j * MAXM + i, part);
+                        if (is_check) {
+                            atomicMax(a.rowdg + j * 2 * MAXM + i, okey(mx));
+                            atomicMin(a.rowdg + j * 2 * MAXM + MAXM + i, okey(mn));
+                        }
+                        __threadfence();
+                        fin = (atomicAdd(a.rowcnt + j * MAXM + i, 1u) == (unsigned)a.T - 1);
+                        if (fin) {
+                            __threadfence();
+                            part = atomicExch(a.rowacc + j * MAXM + i, 0ull);
+                            if (is_check) {
+                                mx = okey_inv(atomicExch(a.rowdg + j * 2 * MAXM + i, 0ull));
+                                mn = okey_inv(atomicExch(a.rowdg + j * 2 * MAXM + MAXM + i, ~0ull));
+                            }
+                            a.rowcnt[j * MAXM + i] = 0u;
+                        }
+                    }
+                    if (fin) {
+                        double r2, r3, s1, s2;
+                        finalize_row(a, cin, i, j, (double)(long long)part * a.fx_inv[i], mx, mn, &r2,
+                                     &r3, &s1, &s2);
+                        my_r2 = fmax(my_r2, r2);
+                        my_r3 = fmax(my_r3, r3);
+                        my_s1 = fmax(my_s1, s1);
+                        my_s2 = fmax(my_s2, s2);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    s_arr[b] = 0u;
+                    __threadfence_block();
+                    atomicAdd(&s_gen[b], 1u);  // release the slot to item litem + UB
+                }
+            }
+            continue;
+        }
         // ---- deterministic block reduction of Sg (sum), dg (max/min) per source
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -628,19 +833,23 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
         __syncthreads();  // red/rowres/k0x reused by the next item
     }
 
-    // ---- per-CTA partials: block max of r1, s3; row maxima of threads < M
+    // ---- per-CTA partials: block max of r1, s3 and of the row terms (held by the
+    // finalising lanes: threads < M, or lanes < M of any warp in the FX variant)
+    __syncthreads();
     if (is_check) {
         my_r1 = warp_max(my_r1);
         my_s3 = warp_max(my_s3);
+        my_r2 = warp_max(my_r2);
+        my_r3 = warp_max(my_r3);
+        my_s1 = warp_max(my_s1);
+        my_s2 = warp_max(my_s2);
         if (lane == 0) {
             red[wid][0] = my_r1;
             red[wid][1] = my_s3;
-        }
-        if (tid < M) {
-            rowres[tid] = my_r2;
-            rowres[M + tid] = my_r3;
-            rowres[2 * M + tid] = my_s1;
-            k0x[tid] = my_s2;
+            red[wid][2] = my_r2;
+            red[wid][3] = my_r3;
+            red[wid][4] = my_s1;
+            red[wid][5] = my_s2;
         }
         __syncthreads();
         if (tid == 0) {
@@ -648,12 +857,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             for (int w = 0; w < nw; ++w) {
                 r1 = fmax(r1, red[w][0]);
                 s3 = fmax(s3, red[w][1]);
-            }
-            for (int i = 0; i < M; ++i) {
-                r2 = fmax(r2, rowres[i]);
-                r3 = fmax(r3, rowres[M + i]);
-                s1 = fmax(s1, rowres[2 * M + i]);
-                s2 = fmax(s2, k0x[i]);
+                r2 = fmax(r2, red[w][2]);
+                r3 = fmax(r3, red[w][3]);
+                s1 = fmax(s1, red[w][4]);
+                s2 = fmax(s2, red[w][5]);
             }
             acc[3 * MAXM + 0] = r1;
             acc[3 * MAXM + 1] = r2;

@@ -81,24 +81,7 @@ __device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// order-preserving map double -> uint64 (max/min of keys = max/min of values)
-__device__ __forceinline__ unsigned long long okey(double x) {
-    const unsigned long long u = (unsigned long long)__double_as_longlong(x);
-    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double okey_inv(unsigned long long k) {
-    const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
-    return __longlong_as_double((long long)u);
-}
-
-// exact warp sum of 64-bit two's-complement values (mod 2^64): three 21/21/22-bit
-// limbs, each summed by redux.sync (no carries lost: 32 * 2^22 < 2^32)
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-    const unsigned l0 = __reduce_add_sync(0xffffffffu, (unsigned)(v & 0x1FFFFFull));
-    const unsigned l1 = __reduce_add_sync(0xffffffffu, (unsigned)((v >> 21) & 0x1FFFFFull));
-    const unsigned l2 = __reduce_add_sync(0xffffffffu, (unsigned)(v >> 42));
-    return (unsigned long long)l0 + ((unsigned long long)l1 << 21) + ((unsigned long long)l2 << 42);
-}
+// okey / okey_inv / warp_sum_u64: admm_kernels.cuh
 
 // (6c) x1^{(i)} = (1/q_total) sum_j c^{(i,j)} over one publication buffer
 // [M][q] (reading G1: the mean).  Warp-collective; every lane returns the same
