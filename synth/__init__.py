@@ -13,7 +13,14 @@ run would have.
 
 from .phev import (  # noqa: F401
     BASE_SEED,
+    DELTA_E,
+    E0_FRAC,
+    E_MAX,
+    EN_FRAC,
+    battery_loss_coeffs,
     phev_problem,
+    realised_drive,
+    supervisor_problem,
     toy_problem,
     horizon_problem,
     random_problem,

@@ -222,3 +222,36 @@ def random_problem(m: int, n: int, q: int, seed: int, scale: float = 1.0,
     c = gx.sum(axis=2).max(axis=1) + cap_slack * n * scale
     return dict(m=m, n=n, q=q, a2=a2, a1=a1, a0=a0, b2=b2, b1=b1, b0=b0,
                 lo=lo, hi=hi, y=y, c=c)
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 2 (shrinking-horizon supervisory control) data
+SUPERVISOR_SAMPLE_BASE = 1 << 20  # scenario streams of instant t: j = BASE + t * 4096 + r
+TRUE_STREAM = (1 << 20) - 1       # the realised drive (one extra stream)
+
+
+def supervisor_problem(N: int, q: int, t: int, delta_e: float, seed: int = BASE_SEED):
+    """Step-1/2 data of Algorithm 2 at sampling instant t of an N-step trip:
+    q fresh demand / speed samples of the remaining horizon k = t..N-1
+    (n = N - t), engine and battery maps from the sampled speeds, and the
+    battery capacity c2 = dE = E_t - E_n."""
+    if not 0 <= t < N:
+        raise ValueError("t must be in [0, N)")
+    y, w = scenarios(N, SUPERVISOR_SAMPLE_BASE + t * 4096, q, seed)
+    y = np.ascontiguousarray(y[:, t:])
+    w = np.ascontiguousarray(w[:, t:])
+    return _assemble(y, w, [dict(kind="engine", cap=np.inf),
+                            dict(kind="storage", cap=float(delta_e))], N - t, q)
+
+
+def realised_drive(N: int, seed: int = BASE_SEED):
+    """The drive that actually happens (demand y[N], speed w[N]): one more
+    independent sample of the same distribution."""
+    y, w = scenarios(N, TRUE_STREAM, 1, seed)
+    return y[0].copy(), w[0].copy()
+
+
+def battery_loss_coeffs(w):
+    """b2 of the battery map g = x + b2 x^2 at engine speed w (same map as the
+    storage source of _assemble)."""
+    return 1e-6 * (0.8 + 0.4 * np.asarray(w) / 4500.0)
