@@ -812,7 +812,7 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
         cudaGetLastError();
-    double frac = 0.6;
+    double frac = 0.4;  // measured best for PHEV q=50 (profiles/README.md)
     if (const char* e = getenv("ADMM_TILE0_FRAC")) frac = atof(e);
     long long T0 = std::max<long long>(1, std::min<long long>(ONCHIP_MAX_T, (sms + q - 1) / q));
     T0 = std::min<long long>(T0, std::max<long long>(1, n / 32));
@@ -831,7 +831,7 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
         if (smem > 200 * 1024 || TCM > 4 * 512) continue;
         const long long G = q * T;
         if (G > 32LL * sms) continue;
-        const int nbw = (int)std::min<long long>(16, (TCM + 31) / 32);
+        const int nbw = (int)std::min<long long>(ONCHIP_MAX_WARPS - 1, (TCM + 31) / 32);
         const int BS = (nbw + 1) * 32;
         if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess) {

@@ -248,6 +248,58 @@ __device__ __forceinline__ void gs_cell_prep(const double* a2q, const double* a1
     }
 }
 
+// gs_cell_prep on two cells (c[0], c[1]) of one thread with interleaved chains
+// (on-chip engines).  Coefficients are read from the shared-memory tile (row
+// stride TCM) where they are used, which keeps the two-cell register footprint
+// small; xo/xn are [M][2].  Never the consensus cell.
+template <int M, int MODE>
+__device__ __forceinline__ void gs_cell2_smem(const double* s_a2q, const double* s_a1q,
+                                              const double* s_b2, const double* s_b1,
+                                              const double* s_bq, const double* s_ib,
+                                              const double* s_lo, const double* s_hi, int TCM,
+                                              const int* c, const double (*xo)[2], double (*xn)[2],
+                                              const double* y, const double* s_e,
+                                              const double* mu_e, const double* zl,
+                                              const double* R) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double C[2], D[2], cn[2], dn[2], bn[2], lo[2], hi[2];
+        bool quart[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int e = i * TCM + c[u];
+            double others = 0.0;
+#pragma unroll
+            for (int l = 0; l < M; ++l)
+                if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
+            const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
+            const double xoi = xo[i][u];
+            const double b2 = s_b2[e], b1 = s_b1[e];
+            const double ee = fma(fma(b2, xoi, b1), xoi, zl[i]);
+            C[u] = fma(0.5 * R[0], fma(b1, b1, -2.0 * b2 * ee), s_a2q[e] + 0.5 * R[1]);
+            D[u] = fma(-R[0] * b1, ee, fma(-R[1], phi, s_a1q[e]));
+            quart[u] = (b2 != 0.0);
+            const double ia2 = s_ib[e] * R[3];
+            bn[u] = s_bq[e];
+            cn[u] = C[u] * ia2;
+            dn[u] = 0.5 * D[u] * ia2;
+            lo[u] = s_lo[e];
+            hi[u] = s_hi[e];
+        }
+        if (quart[0] && quart[1]) {
+            double r[2];
+            quartic_core2<MODE>(bn, cn, dn, C, D, lo, hi, r);
+            xn[i][0] = r[0];
+            xn[i][1] = r[1];
+        } else {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                xn[i][u] = quart[u] ? quartic_core<MODE>(bn[u], cn[u], dn[u], C[u], D[u], lo[u], hi[u])
+                                    : clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
+        }
+    }
+}
+
 // (6e)/(6f) for one cell with the reduced state v = s - mu (identity I2);
 // returns v_new and updates the check maxima |s - sum x + y| and
 // |(s - s~) - sum_i (x - x~)|.

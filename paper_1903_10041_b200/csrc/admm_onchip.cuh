@@ -43,7 +43,7 @@ namespace admm_dev {
 
 constexpr unsigned long long PUB_EMPTY = 0xFFF4DEADBEEF0001ull;  // sNaN payload: never computed
 constexpr int PUB_BUFS = 4;
-constexpr int ONCHIP_MAX_WARPS = 17;     // 16 bulk warps + 1 consensus warp
+constexpr int ONCHIP_MAX_WARPS = 16;     // 15 bulk warps + 1 consensus warp (128 regs)
 constexpr int ONCHIP_MAX_T = 16;         // tiles (CTAs) per cluster
 constexpr int CHK_SLOTS = 6 + 2 * MAXM;  // r1 r2 r3 s1 s2 s3 | max_j x_1 [MAXM] | min_j x_1 [MAXM]
 
@@ -298,32 +298,76 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
         }
         double my_r1 = 0.0, my_s3 = 0.0;
         if (!cons_warp) {
-            // ---- bulk cells: every cell of the tile except the consensus cell k = 0
-            for (int cc = tid; cc < ncell; cc += nbt) {
-                if (k0 + cc == 0) continue;
-                double a2q[M], a1q[M], cb2[M], cb1[M], bq[M], ib[M], clo[M], chi[M], xo[M], xn[M],
-                    dummy[M];
+            // ---- bulk cells: every cell of the tile except the consensus cell k = 0.
+            // Pairs (cc, cc + nbt) go through the interleaved two-cell chain.
+            for (int cc = tid; cc < ncell; cc += 2 * nbt) {
+                const int c2 = cc + nbt;
+                const bool two = (c2 < ncell) && (k0 + cc != 0);
+                if (two) {
+                    const int cs2[2] = {cc, c2};
+                    double xo[M][2], xn[M][2], yy[2], vv[2], se[2], me[2];
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    const int e = i * TCM + cc;
-                    a2q[i] = s_a2q[e]; a1q[i] = s_a1q[e]; cb2[i] = s_b2[e]; cb1[i] = s_b1[e];
-                    bq[i] = s_bq[e]; ib[i] = s_ib[e]; clo[i] = s_lo[e]; chi[i] = s_hi[e];
-                    xo[i] = s_x[e];
-                    dummy[i] = 0.0;
+                    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                        for (int i = 0; i < M; ++i) xo[i][u] = s_x[i * TCM + cs2[u]];
+                        vv[u] = s_v[cs2[u]];
+                        yy[u] = s_y[cs2[u]];
+                        se[u] = fmax(vv[u], 0.0);
+                        me[u] = vv[u] < 0.0 ? -vv[u] : 0.0;
+                    }
+                    gs_cell2_smem<M, MODE>(s_a2q, s_a1q, s_b2, s_b1, s_bq, s_ib, s_lo, s_hi, TCM, cs2,
+                                           xo, xn, yy, se, me, zl, R);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int c = cs2[u];
+                        double txo[M], txn[M];
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            txo[i] = xo[i][u];
+                            txn[i] = xn[i][u];
+                        }
+                        s_v[c] = cell_tail<M>(txo, txn, yy[u], vv[u], 1.0, is_check, my_r1, my_s3);
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            const double b2 = s_b2[i * TCM + c], b1 = s_b1[i * TCM + c];
+                            s_x[i * TCM + c] = txn[i];
+                            fx[i] += __double2ll_rn(fma(b2, txn[i], b1) * txn[i] * fxs[i]);
+                            if (is_check) {
+                                const double dg = (txn[i] - txo[i]) * fma(b2, txn[i] + txo[i], b1);
+                                dgx[i] = fmax(dgx[i], dg);
+                                dgn[i] = fmin(dgn[i], dg);
+                            }
+                        }
+                    }
+                    continue;
                 }
-                const double vv = s_v[cc];
-                const double yy = s_y[cc];
-                gs_cell_prep<M, MODE>(a2q, a1q, cb2, cb1, bq, ib, clo, chi, xo, xn, yy, fmax(vv, 0.0),
-                                      vv < 0.0 ? -vv : 0.0, zl, R, false, dummy);
-                s_v[cc] = cell_tail<M>(xo, xn, yy, vv, 1.0, is_check, my_r1, my_s3);
+#pragma unroll 1
+                for (int c = cc; c < ncell && c <= cc + nbt; c += nbt) {
+                    if (k0 + c == 0) continue;
+                    double a2q[M], a1q[M], cb2[M], cb1[M], bq[M], ib[M], clo[M], chi[M], xo[M], xn[M],
+                        dummy[M];
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    s_x[i * TCM + cc] = xn[i];
-                    fx[i] += __double2ll_rn(fma(cb2[i], xn[i], cb1[i]) * xn[i] * fxs[i]);
-                    if (is_check) {
-                        const double dg = (xn[i] - xo[i]) * fma(cb2[i], xn[i] + xo[i], cb1[i]);
-                        dgx[i] = fmax(dgx[i], dg);
-                        dgn[i] = fmin(dgn[i], dg);
+                    for (int i = 0; i < M; ++i) {
+                        const int e = i * TCM + c;
+                        a2q[i] = s_a2q[e]; a1q[i] = s_a1q[e]; cb2[i] = s_b2[e]; cb1[i] = s_b1[e];
+                        bq[i] = s_bq[e]; ib[i] = s_ib[e]; clo[i] = s_lo[e]; chi[i] = s_hi[e];
+                        xo[i] = s_x[e];
+                        dummy[i] = 0.0;
+                    }
+                    const double vv = s_v[c];
+                    const double yy = s_y[c];
+                    gs_cell_prep<M, MODE>(a2q, a1q, cb2, cb1, bq, ib, clo, chi, xo, xn, yy, fmax(vv, 0.0),
+                                          vv < 0.0 ? -vv : 0.0, zl, R, false, dummy);
+                    s_v[c] = cell_tail<M>(xo, xn, yy, vv, 1.0, is_check, my_r1, my_s3);
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        s_x[i * TCM + c] = xn[i];
+                        fx[i] += __double2ll_rn(fma(cb2[i], xn[i], cb1[i]) * xn[i] * fxs[i]);
+                        if (is_check) {
+                            const double dg = (xn[i] - xo[i]) * fma(cb2[i], xn[i] + xo[i], cb1[i]);
+                            dgx[i] = fmax(dgx[i], dg);
+                            dgn[i] = fmin(dgn[i], dg);
+                        }
                     }
                 }
             }
