@@ -1562,7 +1562,7 @@ const char* admm_build_info(void) {
 }  // extern "C"
 
 #ifdef ADMM_PHASE_PROF
-extern "C" int admm_debug_phase(unsigned long long* out16) {
-    return cudaMemcpyFromSymbol(out16, admm_dev::g_phase, sizeof(admm_dev::g_phase)) == cudaSuccess ? 0 : 1;
+extern "C" int admm_debug_phase(unsigned long long* out24) {
+    return cudaMemcpyFromSymbol(out24, admm_dev::g_phase, sizeof(admm_dev::g_phase)) == cudaSuccess ? 0 : 1;
 }
 #endif

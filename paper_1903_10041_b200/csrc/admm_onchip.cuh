@@ -48,7 +48,7 @@ constexpr int ONCHIP_MAX_T = 16;         // tiles (CTAs) per cluster
 constexpr int CHK_SLOTS = 6 + 2 * MAXM;  // r1 r2 r3 s1 s2 s3 | max_j x_1 [MAXM] | min_j x_1 [MAXM]
 
 #ifdef ADMM_PHASE_PROF  // development build only: per-phase clock64() totals of CTA 0
-__device__ unsigned long long g_phase[2][8];
+__device__ unsigned long long g_phase[3][8];
 #define PHASE(k)                                  \
     if (prof_on) {                                \
         const unsigned long long _c = clock64();  \
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     __syncthreads();
     cluster.sync();  // mates' shared memory is live before any DSMEM access
 #ifdef ADMM_PHASE_PROF
-    const bool prof_on = blockIdx.x == 0 && (tid == 0 || tid == nbt);
+    const bool prof_on = (blockIdx.x == 0 && (tid == 0 || tid == nbt)) || (blockIdx.x == 1 && tid == 0);
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last = clock64();
 #endif
 
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                 }
             }
             x1_known = false;
+            PHASE(2)
             // reset this row's slots of the buffer iteration it+1 publishes into
             if (lane == 0)
 #pragma unroll
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                         st_relaxed_u64(p.pub + ((size_t)(it & (PUB_BUFS - 1)) * a.m + i) * qq + j,
                                        (unsigned long long)__double_as_longlong(xk0[i] - cnu[i]));
                 }
+                PHASE(3)
                 s_v[0] = cell_tail<M>(xo, xk0, yy, vv, 1.0, is_check, my_r1, my_s3);
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     }
 #ifdef ADMM_PHASE_PROF
     if (prof_on)
-        for (int k = 0; k < 8; ++k) g_phase[tid == 0 ? 0 : 1][k] = ph_acc[k];
+        for (int k = 0; k < 8; ++k) g_phase[blockIdx.x == 1 ? 2 : (tid == 0 ? 0 : 1)][k] = ph_acc[k];
 #endif
     // ---- (6h) of the last iteration if it was not a check, then write back
     if (cons_warp && tile == 0 && !x1_known) {

@@ -47,9 +47,15 @@ def compare_states(P, So, Sg, tol=1e-9):
 
 
 # streaming sweep + graph while loop; persistent with rows in clusters; persistent
-# with a grid barrier per iteration (forced through ADMM_PERSIST_GRID=1)
+# with a grid barrier per iteration (forced through ADMM_PERSIST_GRID=1); the
+# barrier-free fixed-point sweep on every shape (ADMM_SWEEP_FX=1) and the opt-in
+# TMA-pipelined sweep (ADMM_STREAM_TMA=1)
 ENGINES = ["stream", "cluster", "grid"]
-_EXEC = {"stream": 1, "cluster": 2, "grid": 2, 0: 0}
+ALT_ENGINES = ["stream_fx", "stream_tma"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_fx": 1, "stream_tma": 1, 0: 0}
+_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_fx": {"ADMM_SWEEP_FX": "1"},
+        "stream_tma": {"ADMM_STREAM_TMA": "1"}}
+_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA")
 
 
 def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_iter=None,
@@ -63,10 +69,9 @@ def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_it
                      exec_mode=_EXEC[engine])
     import os
 
-    if engine == "grid":
-        os.environ["ADMM_PERSIST_GRID"] = "1"
-    else:
-        os.environ.pop("ADMM_PERSIST_GRID", None)
+    for k in _ENV_KEYS:
+        os.environ.pop(k, None)
+    os.environ.update(_ENV.get(engine, {}))
     s.set_problem(P)
     info = None
     if mode == "iterate":
@@ -77,7 +82,8 @@ def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_it
     x, x1, sol = s.solution()
     hist = s.history()
     s.close()
-    os.environ.pop("ADMM_PERSIST_GRID", None)
+    for k in _ENV_KEYS:
+        os.environ.pop(k, None)
     return S, sol if info is None else {**sol, **info}, hist
 
 
@@ -124,7 +130,7 @@ def test_toy_fixed_iterations(iters, engine):
 
 
 @pytest.mark.parametrize("iters", [1, 10, 200])
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + ALT_ENGINES)
 def test_phev_q50_fixed_iterations(iters, engine):
     P = synth.phev_problem(1000, 50)
     prm = oracle.default_params(r_bar=1e-6 * P["c"][1])
@@ -137,7 +143,7 @@ def test_phev_q50_fixed_iterations(iters, engine):
 @pytest.mark.parametrize("m,n,q", [(1, 1, 1), (2, 37, 3), (3, 1000, 4), (4, 1023, 2),
                                    (2, 1025, 3), (2, 2500, 2), (4, 3001, 1), (1, 4, 7)])
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + ALT_ENGINES)
 def test_random_fixed_iterations(m, n, q, mode, engine):
     """Ragged tails (n not a multiple of the tile / of 4), multi-tile rows
     (n > 1024), every m the library instantiates, both box modes."""
@@ -150,7 +156,7 @@ def test_random_fixed_iterations(m, n, q, mode, engine):
     check_hist(ho, hg, P, So)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + ALT_ENGINES)
 def test_horizon_m4_multitile(engine):
     P = synth.horizon_problem(10000)
     prm = oracle.default_params(r_bar=1e-6 * P["c"][2])
@@ -173,7 +179,7 @@ def test_infinite_bounds_and_capacities(engine):
 
 
 # --------------------------------------------------------------- convergence
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + ALT_ENGINES)
 def test_phev_q50_solve_to_tolerance(engine):
     """BASELINE.json configs[1]: PHEV m=2, n=1000, q=50 solved to the paper's
     thresholds (r_bar = 1e-6 dE, sigma_bar = 1e-2)."""
