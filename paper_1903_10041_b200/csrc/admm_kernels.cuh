@@ -797,6 +797,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
                 red[wid][3 * i + 2] = dgn[i];
             }
         }
+        __syncwarp();
         __syncthreads();
         if (wid == 0) {
 #pragma unroll
@@ -816,6 +817,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
                 }
             }
         }
+        __syncwarp();
         __syncthreads();
 
         // ---- row finalisation (6b),(6g),(6d),(6i)
@@ -837,9 +839,11 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
                 __stcg(rp + 2, rowres[3 * tid + 2]);
             }
             __threadfence();
-            __syncthreads();
+            __syncwarp();
+        __syncthreads();
             if (tid == 0) s_last = (atomicAdd(a.row_cnt + j, 1) == a.T - 1);
-            __syncthreads();
+            __syncwarp();
+        __syncthreads();
             if (s_last) {
                 __threadfence();
                 // tile partials of row j: lane-strided loads (all in flight), fixed-order
@@ -882,6 +886,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             acc[MAXM + tid] = fmax(acc[MAXM + tid], k0x[tid]);
             acc[2 * MAXM + tid] = fmin(acc[2 * MAXM + tid], k0x[tid]);
         }
+        __syncwarp();
         __syncthreads();  // red/rowres/k0x reused by the next item
     }
 

@@ -1,0 +1,27 @@
+"""Small runs of every engine for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_1903_10041_b200 as L, synth
+
+cases = [("toy", synth.toy_problem()), ("phev q3 n200", synth.phev_problem(200, 3)),
+         ("random m3 n37 q3", synth.random_problem(3, 37, 3, seed=5)),
+         ("random m2 n1025 q2", synth.random_problem(2, 1025, 2, seed=6))]
+engines = [("stream", 1, {}), ("cluster", 2, {}), ("grid", 2, {"ADMM_PERSIST_GRID": "1"}),
+           ("stream_fx", 1, {"ADMM_SWEEP_FX": "1"}), ("stream_tma", 1, {"ADMM_STREAM_TMA": "1"})]
+only = os.environ.get("ENGINES")
+for name, P in cases:
+    for en, mode, env in engines:
+        if only and en not in only.split(","):
+            continue
+        for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        s = L.AdmmSolver(P["m"], P["n"], P["q"], r_bar=1e-6 * max(1.0, float(np.nanmax(np.where(np.isfinite(P["c"]), P["c"], 0)))), exec_mode=mode)
+        s.set_problem(P)
+        s.iterate(25)
+        S = s.state()
+        print(name, en, L._lib.ENGINE_NAMES[s.engine()[0]], "x finite", bool(np.isfinite(S["x"]).all()), flush=True)
+        s.close()
+x = L.quartic_minimize_batch(*[__import__("torch").rand(1000, dtype=__import__("torch").float64, device="cuda") + 0.1 for _ in range(4)])
+print("quartic ok", bool(__import__("torch").isfinite(x).all()))
