@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ph_last = clock64();
 #endif
 
+    // DSMEM address of cluster-mate `lane`'s row accumulators (lanes < T), mapped once
+    unsigned long long* mate_acc =
+        lane < T ? cluster.map_shared_rank(&s_acc[0][0], lane) : &s_acc[0][0];
     const long long lim = P.iter_limit;
     int until_chk = ce > 0 ? (int)(ce - 1 - it0 % ce) : -1;  // iterations until the next check
     long long it = it0;
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const unsigned long long ws = warp_sum_u64((unsigned long long)fx[i]);
-            if (lane < T && ws != 0ull) atomicAdd(cluster.map_shared_rank(&s_acc[par][i], lane), ws);
+            if (lane < T && ws != 0ull) atomicAdd(mate_acc + par * M + i, ws);
         }
         double cta_r1 = 0.0, cta_s3 = 0.0;
         if (is_check) {
