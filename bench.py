@@ -45,7 +45,8 @@ def parse():
                     choices=["phev", "toy", "horizon", "sweep", "microbench", "crossover", "qsweep"])
     ap.add_argument("--q", type=int, default=None, help="scenarios per GPU (phev/sweep)")
     ap.add_argument("--n", type=int, default=None, help="horizon (horizon workload)")
-    ap.add_argument("--family", default="R", help="microbench quartic family (R or C)")
+    ap.add_argument("--family", default="C",
+                    help="microbench quartic family: C = convex (BASELINE.json configs[4]) or R")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
@@ -156,7 +157,19 @@ class ClockSampler:
         try:
             rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
         except Exception:
-            return None
+            rows = []
+        if not any(len(r) >= 9 and r[0].strip() == str(device) for r in rows):
+            # timed region shorter than the 100 ms sampling period: one sample right after
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                     "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=20).stdout
+                rows = [r.split(", ") for r in out.strip().splitlines()]
+            except Exception:
+                return None
         rows = [r for r in rows if len(r) >= 9 and r[0].strip() == str(device)]
         if not rows:
             return None
@@ -360,7 +373,8 @@ def run_quartic(args, W, dev, flush):
                clocks=clk.summary(dev.index), gpu_launches=args.steps,
                roof={"bound": "hbm", "kernel": "quartic_batch_vec_kernel", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": ncu_traffic("microbench", "quartic_batch_vec_kernel"),
+                     "traffic": ncu_traffic("microbench_C" if W["family"] == "C" else "microbench",
+                                            "quartic_batch_vec_kernel"),
                      "alg_bytes_per_launch": 56 * N,
                      "avg_launch_ms": avg * 1e3})
     del A, B, C, D, lo, hi
