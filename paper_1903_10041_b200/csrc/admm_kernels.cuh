@@ -542,65 +542,44 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
 
     if (FX) __syncthreads();  // slot counters initialised
     long long litem = 0;
-    for (long long item = blockIdx.x; item < nitems; item += a.G, ++litem) {
-        const long long j = item / a.T;
-        const int tile = (int)(item - j * a.T);
-        {
-            // L2 prefetch of the next item's streams (one bulk prefetch per stream row),
-            // so its loads hit L2 instead of exposing HBM latency at the item start
-            const long long nx = item + a.G;
-            if (nx < nitems && tid < 5 * M + 2) {
-                const long long jn = nx / a.T;
-                const int kn = (int)(nx - jn * a.T) * a.tile;
-                const int nc = min(a.tile, a.n_pad - kn);
-                const unsigned bytes = (unsigned)(nc * 8) & ~15u;
-                const double* src;
-                if (tid < 5 * M) {
-                    const int i = tid / 5, s5 = tid - 5 * (tid / 5);
-                    const double* base = s5 == 0 ? a.x : s5 == 1 ? a.a2 : s5 == 2 ? a.a1 : s5 == 3 ? a.b2 : a.b1;
-                    src = base + (long long)i * qn + jn * a.n_pad + kn;
-                } else {
-                    src = (tid == 5 * M ? a.y : a.v) + jn * a.n_pad + kn;
-                }
-                if (bytes)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-            }
-        }
+    // (row, tile) of the item, advanced incrementally (no 64-bit division per item)
+    long long j = (long long)blockIdx.x / a.T;
+    int tile = (int)((long long)blockIdx.x - j * a.T);
+    const int gT = a.G / a.T, gR = a.G - gT * a.T;  // G = gT * T + gR
+    double x1c[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) x1c[i] = cin.x1[i];
+    const bool nu_pending = cin.nu_pending != 0;
+    for (long long item = blockIdx.x; item < nitems; item += a.G, ++litem,
+                   j += gT + ((tile += gR) >= a.T ? 1 : 0), tile -= (tile >= a.T ? a.T : 0)) {
         const int k = tile * a.tile + CPT * tid;  // first of this thread's 2 cells
         const bool inb = k < a.n_pad;             // n_pad % 4 == 0: both cells in bounds
         const bool v0 = k < a.n, v1 = (k + 1) < a.n;
+        const int kl = inb ? k : 0;  // out-of-range threads load cell 0 (results discarded)
 
         double xo[M][2], xn[M][2];
         double Sg[M], dgx[M], dgn[M];
-        double yv[2] = {0, 0}, vv[2] = {0, 0};
-        if (inb) {
-            const double2 t2 = __ldg(reinterpret_cast<const double2*>(a.y + j * a.n_pad + k));
+        double yv[2], vv[2];
+        {
+            const double2 t2 = __ldg(reinterpret_cast<const double2*>(a.y + j * a.n_pad + kl));
             yv[0] = t2.x; yv[1] = t2.y;
-            const double2 u2 = *(reinterpret_cast<const double2*>(a.v + j * a.n_pad + k));
+            const double2 u2 = *(reinterpret_cast<const double2*>(a.v + j * a.n_pad + kl));
             vv[0] = u2.x; vv[1] = u2.y;
         }
         // coefficient streams, all issued up front
         double ca2[M][2], ca1[M][2], cb2[M][2], cb1[M][2], clo[M][2], chi[M][2];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            if (inb) {
-                const long long e = (long long)i * qn + j * a.n_pad + k;
-                double2 t;
-                t = *(reinterpret_cast<const double2*>(a.x + e));  xo[i][0] = t.x; xo[i][1] = t.y;
-                t = __ldg(reinterpret_cast<const double2*>(a.a2 + e)); ca2[i][0] = t.x; ca2[i][1] = t.y;
-                t = __ldg(reinterpret_cast<const double2*>(a.a1 + e)); ca1[i][0] = t.x; ca1[i][1] = t.y;
-                t = __ldg(reinterpret_cast<const double2*>(a.b2 + e)); cb2[i][0] = t.x; cb2[i][1] = t.y;
-                t = __ldg(reinterpret_cast<const double2*>(a.b1 + e)); cb1[i][0] = t.x; cb1[i][1] = t.y;
-                const long long bk = (long long)i * a.n_pad + k;
-                t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
-                t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
-            } else {
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    xo[i][c] = 0; ca2[i][c] = 0; ca1[i][c] = 0; cb2[i][c] = 0; cb1[i][c] = 0;
-                    clo[i][c] = 0; chi[i][c] = 0;
-                }
-            }
+            const long long e = (long long)i * qn + j * a.n_pad + kl;
+            double2 t;
+            t = *(reinterpret_cast<const double2*>(a.x + e));  xo[i][0] = t.x; xo[i][1] = t.y;
+            t = __ldg(reinterpret_cast<const double2*>(a.a2 + e)); ca2[i][0] = t.x; ca2[i][1] = t.y;
+            t = __ldg(reinterpret_cast<const double2*>(a.a1 + e)); ca1[i][0] = t.x; ca1[i][1] = t.y;
+            t = __ldg(reinterpret_cast<const double2*>(a.b2 + e)); cb2[i][0] = t.x; cb2[i][1] = t.y;
+            t = __ldg(reinterpret_cast<const double2*>(a.b1 + e)); cb1[i][0] = t.x; cb1[i][1] = t.y;
+            const long long bk = (long long)i * a.n_pad + kl;
+            t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
+            t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
         }
         // per-row scalars (uniform loads)
         double lam_e[M], zeta_o[M], nu_e[M];
@@ -618,7 +597,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
                 const long long rix = (long long)i * a.q + j;
                 double nu = __ldcg(a.nu + rix);
                 // lazy (6h) of the previous iteration, then its dual rescale
-                if (cin.nu_pending) nu = nu + cin.x1[i] - xo[i][0];
+                if (nu_pending) nu = nu + x1c[i] - xo[i][0];
                 nu_e[i] = nu * f[3];
                 __stcg(a.nu + rix, nu_e[i]);
             }
@@ -629,7 +608,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             zl[i] = zeta_o[i] + lam_e[i];
-            x1nu[i] = cin.x1[i] + nu_e[i];
+            x1nu[i] = x1c[i] + nu_e[i];
         }
         double vn[2];
         {
