@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="horizon (horizon workload)")
     ap.add_argument("--family", default="C",
                     help="microbench quartic family: C = convex (BASELINE.json configs[4]) or R")
+    ap.add_argument("--coeff-bits", type=int, default=64, choices=[64, 32],
+                    help="F2: storage precision of a2,a1,b2,b1 (32 = fp32 coefficients, fp64 math)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
@@ -99,11 +101,13 @@ def workload(args, rank, world):
     raise ValueError(w)
 
 
-def alg_bytes_per_iter(m, n, q):
+def alg_bytes_per_iter(m, n, q, coeff_bits=64):
     """Algorithmic bytes one sweep must move (SURVEY.md
     §8(d)): per element a2,a1,b2,b1 + x read/write; per cell y + v read/write;
-    per (i,k) lo,hi; per row lam,zeta,h,p read+write, sum b0, nu read/write."""
-    return 8 * (6 * m * q * n + 3 * q * n + 2 * m * n + 11 * m * q)
+    per (i,k) lo,hi; per row lam,zeta,h,p read+write, sum b0, nu read/write.
+    F2 (coeff_bits=32): the four coefficients are 4 bytes each."""
+    cb = 4 * (coeff_bits // 8)
+    return cb * m * q * n + 8 * (2 * m * q * n + 3 * q * n + 2 * m * n + 11 * m * q)
 
 
 def measured_peaks():
@@ -207,7 +211,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist = L.make_dist(q_total)
     s = L.AdmmSolver(m, n, q_total, device=local_rank, dist=dist, r_bar=W["r_bar"],
-                     sigma_bar=W["sigma_bar"])
+                     sigma_bar=W["sigma_bar"], coeff_bits=args.coeff_bits)
     s.set_problem(P)
 
     def step():
@@ -257,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
     it_per_s = tot_iters / T
     # dominant kernel: the engine's kernel (ncu launch list: profiles/).  Streaming: one
     # launch = one iteration; persistent engines: one launch = the whole call.
-    ab = alg_bytes_per_iter(m, n, q_loc)
+    ab = alg_bytes_per_iter(m, n, q_loc, args.coeff_bits)
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs")
     peak = hbm if hbm else 6650.0
@@ -586,9 +590,11 @@ def main():
                    else "ADMM element-updates/s (m*n*q x iterations/s; iterations/s alongside)"),
         "value": res["value"], "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["T"] * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.coeff_bits == 64 else "f64 (a2,a1,b2,b1 stored f32: F2)",
         "data": "synthetic (seeded PHEV-shaped generator, synth/)",
         "config": {"workload": W["name"], "l2": "flushed (512 MiB write) before each timed step",
+                   "coeff_bits": args.coeff_bits,
                    "parallelism": f"scenario-sharded dp{world}" if world > 1 else "1 GPU"},
         "gpu_launches": res["gpu_launches"], "roofline": res["roof"],
     }

@@ -206,6 +206,20 @@ admm_status admm_get_timing(admm_ctx* ctx, double out[2]);
    ADMM_ERR_INVALID on a NULL context. */
 admm_status admm_get_engine(const admm_ctx* ctx, int32_t* engine, int64_t* launches);
 
+/* F2 mixed precision (the paper ran in fp32).
+   Storage precision of the per-element cost coefficients a2, a1 (f) and b2, b1 (g)
+   that admm_set_problem applies: bits = 64 (default: stored as given) or 32 (each
+   is rounded to the nearest fp32 value; the streaming sweep then reads 16 instead
+   of 32 bytes of coefficients per element).  Every operation and every state
+   array stays fp64, and every engine solves the same problem -- the one whose
+   a2, a1, b2, b1 are the rounded inputs (a0, b0, bounds, demand, c unchanged);
+   admm_get_state/objective refer to that problem.  Changing the precision
+   discards the loaded problem (call admm_set_problem again; iterate/solve
+   return ADMM_ERR_STATE until then).  ADMM_ERR_INVALID for bits not in {32, 64}
+   or a NULL context. */
+admm_status admm_set_coeff_precision(admm_ctx* ctx, int32_t bits);
+admm_status admm_get_coeff_precision(const admm_ctx* ctx, int32_t* bits);
+
 const char* admm_last_error(const admm_ctx* ctx);
 void admm_destroy(admm_ctx* ctx);
 

@@ -76,6 +76,8 @@ _sigs = {
     "admm_get_history": (C.c_int64, [_ctx_p, _vp, C.c_int64]),
     "admm_get_timing": (C.c_int, [_ctx_p, C.c_double * 2]),
     "admm_get_engine": (C.c_int, [_ctx_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "admm_set_coeff_precision": (C.c_int, [_ctx_p, C.c_int32]),
+    "admm_get_coeff_precision": (C.c_int, [_ctx_p, C.POINTER(C.c_int32)]),
     "admm_last_error": (C.c_char_p, [_ctx_p]),
     "admm_destroy": (None, [_ctx_p]),
     "quartic_minimize_batch": (C.c_int, [_vp] * 7 + [C.c_int64, C.c_int32, _vp]),
@@ -232,6 +234,17 @@ def admm_get_engine(ctx):
     e, n = C.c_int32(0), C.c_int64(0)
     _check(ctx, _lib.admm_get_engine(ctx, C.byref(e), C.byref(n)))
     return int(e.value), int(n.value)
+
+
+def admm_set_coeff_precision(ctx, bits: int):
+    """F2: storage precision (64 or 32) of a2, a1, b2, b1 applied by the next set_problem."""
+    return _check(ctx, _lib.admm_set_coeff_precision(ctx, int(bits)))
+
+
+def admm_get_coeff_precision(ctx) -> int:
+    b = C.c_int32(0)
+    _check(ctx, _lib.admm_get_coeff_precision(ctx, C.byref(b)))
+    return int(b.value)
 
 
 def admm_last_error(ctx) -> str:

@@ -40,7 +40,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, total;
+        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, cf, total;
 };
 
 // streaming sweep block size: 2 cells per thread, at most ADMM_SWEEP_BS (default
@@ -99,6 +99,7 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.rowacc = take((size_t)q * MAXM * 8);
     L.rowdg = take((size_t)q * 2 * MAXM * 8);
     L.rowcnt = take((size_t)q * MAXM * 4);
+    L.cf = take(2 * E);  // F2: fp32 a2, a1, b2, b1 [4][m][q][n_pad] (16 B per element)
     L.total = o;
     return L;
 }
@@ -484,6 +485,7 @@ struct admm_ctx {
     bool fx_ok = false;           // fixed-point scales of the row sums valid (finite bounds)
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
     bool use_tma = false;         // streaming engine: TMA-pipelined sweep (else legacy sweep)
+    int coeff_bits = 64;          // F2: storage precision of a2, a1, b2, b1 (64 or 32)
     bool graph_dirty = true;      // problem changed since the graph was captured
     SArgs sa{};
 };
@@ -531,6 +533,19 @@ void upload_params(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     cudaMemcpyAsync(ctx->ws + ctx->L.prm, &d, sizeof(d), cudaMemcpyHostToDevice, ctx->stream);
 }
 
+// F2: round a2, a1, b2, b1 to fp32 (round to nearest even, the cast), keep the
+// rounded values in the fp64 arrays (all engines see one problem) and the fp32 copies
+__global__ void round_coeff_kernel(long long NE, double* a2, double* a1, double* b2, double* b1,
+                                   float* fa2, float* fa1, float* fb2, float* fb1) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NE; t += stride) {
+        const float u2 = __double2float_rn(a2[t]), u1 = __double2float_rn(a1[t]);
+        const float w2 = __double2float_rn(b2[t]), w1 = __double2float_rn(b1[t]);
+        fa2[t] = u2; fa1[t] = u1; fb2[t] = w2; fb1[t] = w1;
+        a2[t] = u2; a1[t] = u1; b2[t] = w2; b1[t] = w1;
+    }
+}
+
 typedef void (*sweep_fn)(KArgs);
 typedef void (*sweep_tma_fn)(KArgs, SArgs);
 
@@ -544,17 +559,23 @@ bool use_fx_sweep(const admm_ctx* ctx) {
     return ctx->fx_ok && ctx->T > 1;
 }
 
-sweep_fn pick_sweep(int m, int mode, bool fx) {
+template <typename CT>
+sweep_fn pick_sweep_t(int m, int mode, bool fx) {
 #define S(MM)                                                                                  \
     if (m == MM) {                                                                             \
-        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true>                   \
-                                         : sweep_kernel<MM, BOX_PROJECT, true>;                \
-        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false>                          \
-                                 : sweep_kernel<MM, BOX_PROJECT, false>;                       \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT>               \
+                                         : sweep_kernel<MM, BOX_PROJECT, true, CT>;            \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT>                      \
+                                 : sweep_kernel<MM, BOX_PROJECT, false, CT>;                   \
     }
     S(1) S(2) S(3) S(4)
 #undef S
     return nullptr;
+}
+
+// f32: F2 mixed-precision sweep (coefficients read from their fp32 copies)
+sweep_fn pick_sweep(int m, int mode, bool fx, bool f32) {
+    return f32 ? pick_sweep_t<float>(m, mode, fx) : pick_sweep_t<double>(m, mode, fx);
 }
 
 sweep_tma_fn pick_sweep_tma(int m, int mode, int* tl, size_t* smem) {
@@ -579,7 +600,7 @@ admm_status plan_stream(admm_ctx* ctx) {
     // HBM peak at q = 1e4..1e5, profiles/README.md), the fp64 chain latency and
     // not the load/compute overlap being the limiter.
     const char* opt = getenv("ADMM_STREAM_TMA");
-    ctx->use_tma = tf && ctx->fx_ok && (opt && opt[0] == '1');
+    ctx->use_tma = tf && ctx->fx_ok && (opt && opt[0] == '1') && ctx->coeff_bits == 64;
     if (!ctx->use_tma) return ADMM_OK;
     if (cudaFuncSetAttribute((const void*)tf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess) {
@@ -654,7 +675,7 @@ admm_status build_graph(admm_ctx* ctx) {
         cudaGraphDestroy(ctx->graph);
         ctx->graph = nullptr;
     }
-    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx));
+    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32);
     if (!fn) return fail(ctx, ADMM_ERR_INVALID, "m must be in 1..4");
     int occ = 0;
     CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, 0));
@@ -948,7 +969,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         if (st != ADMM_OK) return st;
     } else if (ctx->no_graph) {
         // profiling mode (ADMM_NO_GRAPH=1): plain launches, host polls per body
-        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx));
+        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32);
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
@@ -1197,6 +1218,11 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     a.rowacc = (unsigned long long*)(w + L.rowacc);
     a.rowdg = (unsigned long long*)(w + L.rowdg);
     a.rowcnt = (unsigned*)(w + L.rowcnt);
+    {
+        const size_t NE = (size_t)m * ctx->q * ctx->n_pad;
+        float* cf = (float*)(w + L.cf);
+        a.fa2 = cf; a.fa1 = cf + NE; a.fb2 = cf + 2 * NE; a.fb1 = cf + 3 * NE;
+    }
     ctx->vflag = (unsigned long long*)(w + L.vflag);
     ctx->obj_rows = (double*)(w + L.obj_rows);
     if (ctx->world > 1) {
@@ -1256,6 +1282,16 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             snprintf(buf, sizeof buf, "%s at (i=%lld)", kind_msg(kind), t);
         }
         return fail(ctx, (kind == 2 || kind == 3) ? ADMM_ERR_NONCONVEX : ADMM_ERR_INVALID, buf);
+    }
+    // F2: coefficients stored in fp32 -- every engine then solves the problem whose
+    // a2, a1, b2, b1 are the fp32-rounded inputs (double arrays rounded in place, fp32
+    // copies for the streaming sweep); a0, b0, bounds, demand stay fp64
+    if (ctx->coeff_bits == 32) {
+        const long long NE = (long long)ctx->m * ctx->q * ctx->n_pad;
+        round_coeff_kernel<<<grid_for(NE, 256, ctx->sms), 256, 0, ctx->stream>>>(
+            NE, (double*)a.a2, (double*)a.a1, (double*)a.b2, (double*)a.b1, (float*)a.fa2,
+            (float*)a.fa1, (float*)a.fb2, (float*)a.fb1);
+        CKC(cudaGetLastError());
     }
     // fixed-point scales of the row sums (every engine), prepared constants (on-chip engine)
     ctx->prep_ok = false;
@@ -1494,6 +1530,23 @@ admm_status admm_get_engine(const admm_ctx* ctx, int32_t* engine, int64_t* launc
     if (!ctx) return ADMM_ERR_INVALID;
     if (engine) *engine = ctx->last_engine;
     if (launches) *launches = ctx->launches;
+    return ADMM_OK;
+}
+
+admm_status admm_set_coeff_precision(admm_ctx* ctx, int32_t bits) {
+    if (!ctx) return ADMM_ERR_INVALID;
+    if (bits != 64 && bits != 32) return fail(ctx, ADMM_ERR_INVALID, "coefficient precision must be 64 or 32");
+    if (bits != ctx->coeff_bits) {
+        ctx->coeff_bits = bits;
+        ctx->has_problem = false;  // the loaded problem was stored in the other precision
+        ctx->graph_dirty = true;
+    }
+    return ADMM_OK;
+}
+
+admm_status admm_get_coeff_precision(const admm_ctx* ctx, int32_t* bits) {
+    if (!ctx || !bits) return ADMM_ERR_INVALID;
+    *bits = ctx->coeff_bits;
     return ADMM_OK;
 }
 

@@ -81,7 +81,26 @@ struct KArgs {
     unsigned long long *rowacc;  // [q][MAXM]
     unsigned long long *rowdg;   // [q][2 MAXM] ordered keys (checks)
     unsigned *rowcnt;            // [q][MAXM]
+    // F2: fp32 copies of the per-element coefficients, read by the
+    // streaming sweep when the context stores coefficients in fp32 (admm_set_coeff_precision)
+    const float *fa2, *fa1, *fb2, *fb1;          // [m][q][n_pad]
 };
+
+// two consecutive coefficients (k, k+1) of a stream stored as CT, widened to fp64
+template <typename CT>
+__device__ __forceinline__ void ld2(const CT* p, double* o);
+template <>
+__device__ __forceinline__ void ld2<double>(const double* p, double* o) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = t.x;
+    o[1] = t.y;
+}
+template <>
+__device__ __forceinline__ void ld2<float>(const float* p, double* o) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    o[0] = (double)t.x;
+    o[1] = (double)t.y;
+}
 
 // order-preserving map double -> uint64 (max/min of keys = max/min of values)
 __device__ __forceinline__ unsigned long long okey(double x) {
@@ -496,7 +515,9 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
 // per-warp slots and a last-warp finaliser -- no block barrier inside the item
 // loop, so one warp's loads overlap another warp's fp64 work.  FX = false
 // (an infinite bound): fp64 block reductions with barriers.
-template <int M, int MODE, bool FX>
+// CT = float: F2 mixed precision -- a2, a1, b2, b1 read from their fp32 copies
+// (16 instead of 32 bytes per element), every operation in fp64.
+template <int M, int MODE, bool FX, typename CT>
 __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
     const long long it = *(volatile long long*)a.iter;
     const Ctrl& cin = a.ctrl[it & 1];
@@ -573,10 +594,17 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             const long long e = (long long)i * qn + j * a.n_pad + kl;
             double2 t;
             t = *(reinterpret_cast<const double2*>(a.x + e));  xo[i][0] = t.x; xo[i][1] = t.y;
-            t = __ldg(reinterpret_cast<const double2*>(a.a2 + e)); ca2[i][0] = t.x; ca2[i][1] = t.y;
-            t = __ldg(reinterpret_cast<const double2*>(a.a1 + e)); ca1[i][0] = t.x; ca1[i][1] = t.y;
-            t = __ldg(reinterpret_cast<const double2*>(a.b2 + e)); cb2[i][0] = t.x; cb2[i][1] = t.y;
-            t = __ldg(reinterpret_cast<const double2*>(a.b1 + e)); cb1[i][0] = t.x; cb1[i][1] = t.y;
+            if constexpr (sizeof(CT) == 4) {
+                ld2<float>(a.fa2 + e, ca2[i]);
+                ld2<float>(a.fa1 + e, ca1[i]);
+                ld2<float>(a.fb2 + e, cb2[i]);
+                ld2<float>(a.fb1 + e, cb1[i]);
+            } else {
+                ld2<double>(a.a2 + e, ca2[i]);
+                ld2<double>(a.a1 + e, ca1[i]);
+                ld2<double>(a.b2 + e, cb2[i]);
+                ld2<double>(a.b1 + e, cb1[i]);
+            }
             const long long bk = (long long)i * a.n_pad + kl;
             t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
             t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;

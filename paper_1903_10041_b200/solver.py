@@ -36,7 +36,7 @@ class AdmmSolver:
     (or this rank's scenario shard when `dist` is given)."""
 
     def __init__(self, m, n, q_total, device=0, dist=None, stream=None, params=None,
-                 **param_kw):
+                 coeff_bits=64, **param_kw):
         import torch
 
         self.m, self.n, self.q_total = int(m), int(n), int(q_total)
@@ -60,8 +60,19 @@ class AdmmSolver:
             else:
                 setattr(p, k, v)
         _lib.admm_set_params(self.ctx, p)
+        if coeff_bits != 64:
+            _lib.admm_set_coeff_precision(self.ctx, coeff_bits)
 
     # -------------------------------------------------------------- problem
+    def set_coeff_precision(self, bits):
+        """F2: store a2, a1, b2, b1 in fp32 (bits=32) or fp64 (64) from the next
+        set_problem on (include/admm.h: admm_set_coeff_precision)."""
+        _lib.admm_set_coeff_precision(self.ctx, bits)
+
+    @property
+    def coeff_bits(self):
+        return _lib.admm_get_coeff_precision(self.ctx)
+
     def set_problem(self, prob):
         """prob: dict with a2,a1,a0,b2,b1,b0 [m][q][n], lo,hi [m][n], y [q][n],
         c [m] (numpy = host, torch = host or device)."""
