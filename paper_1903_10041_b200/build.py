@@ -34,14 +34,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """out/defines: experimental variants (e.g. -DSWEEP_LB=1024) written next to the
+    product library and loaded with ADMM_SO=<path>; the product build takes neither."""
+    SO = out or globals()["SO"]
+    if not out and not force and up_to_date():
         return SO
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
+           *[f"-D{d}" for d in defines],
            "-o", SO + ".tmp", os.path.join(CSRC, "admm.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -56,5 +60,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=a.D))

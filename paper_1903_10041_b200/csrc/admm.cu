@@ -45,10 +45,11 @@ struct Layout {
 
 // streaming sweep block size: 2 cells per thread, at most ADMM_SWEEP_BS (default
 // 512: one row per item; 256 splits rows over two CTAs and measured 30 % vs 44 %)
-int pick_bs(long long n) {
-    long long cap = 512;
-    if (const char* e = getenv("ADMM_SWEEP_BS")) cap = std::max(32LL, std::min(512LL, atoll(e)));
-    long long need = (n + CPT - 1) / CPT;
+// cpt = cells per thread (2, or 4 with 256-thread CTAs: same 1024-cell tile)
+int pick_bs(long long n, int cpt = CPT) {
+    long long cap = cpt == 4 ? 256 : 512;
+    if (const char* e = getenv("ADMM_SWEEP_BS")) cap = std::max(32LL, std::min(cap, atoll(e)));
+    long long need = (n + cpt - 1) / cpt;
     long long bs = ((need + 31) / 32) * 32;
     return (int)std::max(32LL, std::min(cap, bs));
 }
@@ -486,6 +487,7 @@ struct admm_ctx {
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
     bool use_tma = false;         // streaming engine: TMA-pipelined sweep (else legacy sweep)
     int coeff_bits = 64;          // F2: storage precision of a2, a1, b2, b1 (64 or 32)
+    int cpt = 2;                  // streaming sweep: cells per thread (2, or 4 for m <= 2)
     bool graph_dirty = true;      // problem changed since the graph was captured
     SArgs sa{};
 };
@@ -552,7 +554,25 @@ typedef void (*sweep_tma_fn)(KArgs, SArgs);
 // Barrier-free (fixed-point, last-warp-finalises) sweep for rows spanning several
 // tiles (horizon n = 1e6: 26 -> 34 % of HBM peak); the barrier variant stays for
 // one-tile rows, where it measured faster (44 vs 38 % at q = 1e4, profiles/README.md).
+bool use_pf_sweep(const admm_ctx* ctx) {
+    const char* e = getenv("ADMM_SWEEP_PF");
+    if (!(e && e[0] == '1')) return false;  // opt-in while measured
+    return ctx->fx_ok && ctx->T == 1 && ctx->m <= 2 && ctx->cpt == 2;
+}
+
+size_t pf_smem_bytes(const admm_ctx* ctx) {
+    if (ctx->cpt == 4)  // staged 4-cell sweep: the per-thread slab
+        return (size_t)(ctx->m == 1 ? Slab4<1>::NF : Slab4<2>::NF) * ctx->bs * 4 * 8;
+    if (!use_pf_sweep(ctx)) return 0;
+    const size_t per = ctx->coeff_bits == 32 ? (size_t)PFCfg<2, float>::PER_THREAD
+                                             : (size_t)PFCfg<2, double>::PER_THREAD;
+    const size_t per1 = ctx->coeff_bits == 32 ? (size_t)PFCfg<1, float>::PER_THREAD
+                                              : (size_t)PFCfg<1, double>::PER_THREAD;
+    return 2 * (size_t)ctx->bs * (ctx->m == 1 ? per1 : per);
+}
+
 bool use_fx_sweep(const admm_ctx* ctx) {
+    if (use_pf_sweep(ctx)) return true;
     const char* e = getenv("ADMM_SWEEP_FX");
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return ctx->fx_ok;
@@ -560,23 +580,38 @@ bool use_fx_sweep(const admm_ctx* ctx) {
 }
 
 template <typename CT>
-sweep_fn pick_sweep_t(int m, int mode, bool fx) {
-#define S(MM)                                                                                  \
+sweep_fn pick_sweep_t(int m, int mode, bool fx, bool pf, int cpt) {
+#define S(MM, UU)                                                                              \
     if (m == MM) {                                                                             \
-        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT>               \
-                                         : sweep_kernel<MM, BOX_PROJECT, true, CT>;            \
-        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT>                      \
-                                 : sweep_kernel<MM, BOX_PROJECT, false, CT>;                   \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, false, UU>    \
+                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, false, UU>; \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, false, UU>           \
+                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, false, UU>;        \
     }
-    S(1) S(2) S(3) S(4)
+#define SP(MM)                                                                                 \
+    if (m == MM && pf) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, true, 2> \
+                                                : sweep_kernel<MM, BOX_PROJECT, true, CT, true, 2>;
+    if (cpt == 4) {
+        S(1, 4) S(2, 4)
+        return nullptr;
+    }
+    SP(1) SP(2)
+    S(1, 2) S(2, 2) S(3, 2) S(4, 2)
 #undef S
+#undef SP
     return nullptr;
 }
 
-// f32: F2 mixed-precision sweep (coefficients read from their fp32 copies)
-sweep_fn pick_sweep(int m, int mode, bool fx, bool f32) {
-    return f32 ? pick_sweep_t<float>(m, mode, fx) : pick_sweep_t<double>(m, mode, fx);
+// f32: F2 mixed-precision sweep (coefficients read from their fp32 copies); pf: the
+// cp.async-prefetching sweep (one-tile rows, m <= 2; use_pf_sweep); cpt: cells per thread
+sweep_fn pick_sweep(int m, int mode, bool fx, bool f32, bool pf, int cpt) {
+    return f32 ? pick_sweep_t<float>(m, mode, fx, pf, cpt) : pick_sweep_t<double>(m, mode, fx, pf, cpt);
 }
+
+// The prefetching sweep: rows of one tile (n <= 2 * block size), m <= 2, fixed-point
+// row sums (finite boxes).  ADMM_SWEEP_PF=0 turns it off.
+bool use_pf_sweep(const admm_ctx* ctx);
+size_t pf_smem_bytes(const admm_ctx* ctx);
 
 sweep_tma_fn pick_sweep_tma(int m, int mode, int* tl, size_t* smem) {
 #define S(MM)                                                                                  \
@@ -647,7 +682,7 @@ admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
         if (ctx->use_tma)
             tf<<<ctx->sa.G, ctx->sa.TL, smem, st>>>(ctx->ka, ctx->sa);
         else
-            fn<<<ctx->G, ctx->bs, 0, st>>>(ctx->ka);
+            fn<<<ctx->G, ctx->bs, pf_smem_bytes(ctx), st>>>(ctx->ka);
         CKC(cudaGetLastError());
         if (ctx->world > 1) {
             CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, st));
@@ -675,10 +710,13 @@ admm_status build_graph(admm_ctx* ctx) {
         cudaGraphDestroy(ctx->graph);
         ctx->graph = nullptr;
     }
-    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32);
+    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt);
     if (!fn) return fail(ctx, ADMM_ERR_INVALID, "m must be in 1..4");
     int occ = 0;
-    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, 0));
+    const size_t dsm = pf_smem_bytes(ctx);
+    if (dsm > 0)
+        CKC(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, dsm));
     occ = std::max(1, std::min(occ, 32));
     const long long items = ctx->q * ctx->T;
     ctx->G = (int)std::max(1LL, std::min(items, (long long)occ * ctx->sms));
@@ -969,7 +1007,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         if (st != ADMM_OK) return st;
     } else if (ctx->no_graph) {
         // profiling mode (ADMM_NO_GRAPH=1): plain launches, host polls per body
-        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32);
+        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt);
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
@@ -1187,8 +1225,12 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     // kernel arguments
     const Layout& L = ctx->L;
     KArgs& a = ctx->ka;
-    ctx->bs = pick_bs(n);
-    ctx->tile = ctx->bs * CPT;
+    {
+        const char* e = getenv("ADMM_SWEEP_CPT");
+        ctx->cpt = (e && e[0] == '4' && m <= 2) ? 4 : 2;
+    }
+    ctx->bs = pick_bs(n, ctx->cpt);
+    ctx->tile = ctx->bs * ctx->cpt;
     ctx->T = (int)((n + ctx->tile - 1) / ctx->tile);
     a.m = m;
     a.n = (int)n;

@@ -319,6 +319,227 @@ __device__ __forceinline__ void gs_cell2_smem(const double* s_a2q, const double*
     }
 }
 
+// U consecutive values of a stream (U = 2: one 128-bit load, U = 4: two)
+template <typename CT, int U>
+__device__ __forceinline__ void ldU(const CT* p, double* o) {
+#pragma unroll
+    for (int h = 0; h < U; h += 2) ld2<CT>(p + h, o + h);
+}
+// read-write state (x, v): plain (L1-coherent) 128-bit loads
+template <int U>
+__device__ __forceinline__ void ldvU(const double* p, double* o) {
+#pragma unroll
+    for (int h = 0; h < U; h += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(p + h);
+        o[h] = t.x;
+        o[h + 1] = t.y;
+    }
+}
+template <int U>
+__device__ __forceinline__ void stU(double* p, const double* v) {
+#pragma unroll
+    for (int h = 0; h < U; h += 2) *reinterpret_cast<double2*>(p + h) = make_double2(v[h], v[h + 1]);
+}
+
+// Algorithm 1 on U independent cells: when all take the trigonometric branch the U
+// straight-line evaluations interleave (ILP U); results bit-identical to quartic_core.
+template <int MODE, int U>
+__device__ __forceinline__ void quartic_coreU(const double* b, const double* c, const double* d,
+                                              const double* C, const double* D, const double* lo,
+                                              const double* hi, double* out) {
+    double Q[U], R[U], De[U];
+    bool all = true;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const double bb = b[u] * b[u];
+        Q[u] = fma(3.0, c[u], -bb) * (1.0 / 9.0);
+        R[u] = fma(b[u], fma(9.0, c[u], -2.0 * bb), -27.0 * d[u]) * (1.0 / 54.0);
+        De[u] = fma(Q[u] * Q[u], Q[u], R[u] * R[u]);
+        all = all && isfinite(De[u]) && !(De[u] > 0.0) && !(Q[u] == 0.0 && R[u] == 0.0);
+    }
+    if (all) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) out[u] = trig_pick<MODE>(b[u], c[u], d[u], Q[u], R[u], De[u], lo[u], hi[u]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) out[u] = quartic_core<MODE>(b[u], c[u], d[u], C[u], D[u], lo[u], hi[u]);
+    }
+}
+
+// gs_cell2 on U cells (arrays [M][U]); k0 marks cell 0 as the consensus cell
+template <int M, int MODE, int U>
+__device__ __forceinline__ void gs_cellU(const double (*ca2)[U], const double (*ca1)[U],
+                                         const double (*cb2)[U], const double (*cb1)[U],
+                                         const double (*clo)[U], const double (*chi)[U],
+                                         const double (*xo)[U], double (*xn)[U], const double* y,
+                                         const double* s_e, const double* mu_e, const double* zl,
+                                         const double* rho, double iq, bool k0, const double* x1nu) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double C[U], D[U], bn[U], cn[U], dn[U], lo[U], hi[U];
+        bool allq = true, anyq = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double others = 0.0;
+#pragma unroll
+            for (int l = 0; l < M; ++l)
+                if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
+            const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
+            const double xoi = xo[i][u];
+            const double b2 = cb2[i][u], b1 = cb1[i][u];
+            const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
+            C[u] = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i][u], iq, 0.5 * rho[2]));
+            D[u] = fma(-rho[0] * b1, e, fma(ca1[i][u], iq, -rho[2] * phi));
+            if (k0 && u == 0) {
+                C[u] += 0.5 * rho[3];
+                D[u] += -rho[3] * x1nu[i];
+            }
+            const bool qu = (b2 != 0.0);
+            allq = allq && qu;
+            anyq = anyq || qu;
+            const double ia2 = rcp_nr(qu ? rho[0] * b2 * b2 : 1.0);  // 1 / 2A
+            bn[u] = 1.5 * (rho[0] * b2 * b1) * ia2;
+            cn[u] = C[u] * ia2;
+            dn[u] = 0.5 * D[u] * ia2;
+            lo[u] = clo[i][u];
+            hi[u] = chi[i][u];
+        }
+        if (allq) {
+            double r[U];
+            quartic_coreU<MODE, U>(bn, cn, dn, C, D, lo, hi, r);
+#pragma unroll
+            for (int u = 0; u < U; ++u) xn[i][u] = r[u];
+        } else if (!anyq) {  // a source without g (A = B = 0): quadratic for every cell
+#pragma unroll
+            for (int u = 0; u < U; ++u) xn[i][u] = clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                xn[i][u] = (cb2[i][u] != 0.0) ? quartic_core<MODE>(bn[u], cn[u], dn[u], C[u], D[u], lo[u], hi[u])
+                                              : clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
+        }
+    }
+}
+
+// ------------------------------------------- staged 4-cell Gauss-Seidel (U = 4)
+// The per-cell values that live across Algorithm 1 (x old/new, y, v and the
+// normalised cubic of the source being solved) sit in a per-thread shared-memory
+// slab instead of registers, and the coefficient streams are read (L1/L2) where
+// they are used, so the four interleaved trigonometric chains get the register
+// file.  Slab: field f, thread t, cell u at ((f * bs + t) * 4 + u) doubles.
+template <int M>
+struct Slab4 {
+    static constexpr int XO = 0, XN = M, Y = 2 * M, V = 2 * M + 1, BN = 2 * M + 2, CN = 2 * M + 3,
+                         DN = 2 * M + 4, CC = 2 * M + 5, DD = 2 * M + 6, NF = 2 * M + 7;
+};
+__device__ __forceinline__ void rd4(const double* p, double* o) {
+    const double2 t0 = *reinterpret_cast<const double2*>(p), t1 = *reinterpret_cast<const double2*>(p + 2);
+    o[0] = t0.x; o[1] = t0.y; o[2] = t1.x; o[3] = t1.y;
+}
+__device__ __forceinline__ void wr4(double* p, const double* v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+}
+
+// Same arithmetic, in the same order, as gs_cellU<M, MODE, 4> (bit-identical);
+// inputs XO, Y, V in the slab, output XN in the slab.  e0 = j * n_pad + kl.
+template <int M, int MODE, typename CT>
+__device__ __forceinline__ void staged_gs4(const KArgs& a, double* slab, int bs, int tid, long long e0,
+                                           long long qn, long long bk0, const double* zl,
+                                           const double* rho, double iq, bool k0, const double* x1nu,
+                                           double f2) {
+    using SL = Slab4<M>;
+    auto S = [&](int f) { return slab + ((size_t)f * bs + tid) * 4; };
+    const CT *pa2, *pa1, *pb2, *pb1;
+    if constexpr (sizeof(CT) == 4) {
+        pa2 = a.fa2; pa1 = a.fa1; pb2 = a.fb2; pb1 = a.fb1;
+    } else {
+        pa2 = reinterpret_cast<const CT*>(a.a2); pa1 = reinterpret_cast<const CT*>(a.a1);
+        pb2 = reinterpret_cast<const CT*>(a.b2); pb1 = reinterpret_cast<const CT*>(a.b1);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        bool qf[4];
+        bool allq = true, anyq = false;
+        {
+            double b2[4], b1[4], a2[4], a1[4], xoi[4], y[4], v[4], oth[4] = {0.0, 0.0, 0.0, 0.0};
+            const long long e = (long long)i * qn + e0;
+            ldU<CT, 4>(pb2 + e, b2);
+            ldU<CT, 4>(pb1 + e, b1);
+            ldU<CT, 4>(pa2 + e, a2);
+            ldU<CT, 4>(pa1 + e, a1);
+            rd4(S(SL::XO + i), xoi);
+            rd4(S(SL::Y), y);
+            rd4(S(SL::V), v);
+#pragma unroll
+            for (int l = 0; l < M; ++l) {
+                if (l == i) continue;
+                double t[4];
+                rd4(S(l < i ? SL::XN + l : SL::XO + l), t);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) oth[u] += t[u];
+            }
+            double bn[4], cn[4], dn[4], C[4], D[4], xq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double s_e = fmax(v[u], 0.0);
+                const double mu_e = v[u] < 0.0 ? -v[u] * f2 : 0.0;
+                const double phi = ((s_e - oth[u]) + y[u]) + mu_e;
+                const double ee = fma(fma(b2[u], xoi[u], b1[u]), xoi[u], zl[i]);
+                C[u] = fma(0.5 * rho[0], fma(b1[u], b1[u], -2.0 * b2[u] * ee), fma(a2[u], iq, 0.5 * rho[2]));
+                D[u] = fma(-rho[0] * b1[u], ee, fma(a1[u], iq, -rho[2] * phi));
+                if (k0 && u == 0) {
+                    C[u] += 0.5 * rho[3];
+                    D[u] += -rho[3] * x1nu[i];
+                }
+                qf[u] = (b2[u] != 0.0);
+                allq = allq && qf[u];
+                anyq = anyq || qf[u];
+                const double ia2 = rcp_nr(qf[u] ? rho[0] * b2[u] * b2[u] : 1.0);  // 1 / 2A
+                bn[u] = 1.5 * (rho[0] * b2[u] * b1[u]) * ia2;
+                cn[u] = C[u] * ia2;
+                dn[u] = 0.5 * D[u] * ia2;
+            }
+            if (!allq) {  // quadratic cells (A = B = 0) are finished here
+                double lo[4], hi[4];
+                ldU<double, 4>(a.lo + (long long)i * a.n_pad + bk0, lo);
+                ldU<double, 4>(a.hi + (long long)i * a.n_pad + bk0, hi);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xq[u] = qf[u] ? 0.0 : clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
+                wr4(S(SL::XN + i), xq);
+            }
+            if (anyq) {
+                wr4(S(SL::BN), bn);
+                wr4(S(SL::CN), cn);
+                wr4(S(SL::DN), dn);
+                wr4(S(SL::CC), C);
+                wr4(S(SL::DD), D);
+            }
+        }
+        if (anyq) {
+            double bn[4], cn[4], dn[4], C[4], D[4], lo[4], hi[4], r[4];
+            rd4(S(SL::BN), bn);
+            rd4(S(SL::CN), cn);
+            rd4(S(SL::DN), dn);
+            rd4(S(SL::CC), C);
+            rd4(S(SL::DD), D);
+            ldU<double, 4>(a.lo + (long long)i * a.n_pad + bk0, lo);
+            ldU<double, 4>(a.hi + (long long)i * a.n_pad + bk0, hi);
+            if (allq) {
+                quartic_coreU<MODE, 4>(bn, cn, dn, C, D, lo, hi, r);
+                wr4(S(SL::XN + i), r);
+            } else {
+                double xq[4];
+                rd4(S(SL::XN + i), xq);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (qf[u]) xq[u] = quartic_core<MODE>(bn[u], cn[u], dn[u], C[u], D[u], lo[u], hi[u]);
+                wr4(S(SL::XN + i), xq);
+            }
+        }
+    }
+}
+
 // (6e)/(6f) for one cell with the reduced state v = s - mu (identity I2);
 // returns v_new and updates the check maxima |s - sum x + y| and
 // |(s - s~) - sum_i (x - x~)|.
@@ -488,6 +709,76 @@ __device__ void finalize_global(const KArgs& a, const double* agg, int world, lo
     }
 }
 
+// ------------------------------------------------- per-thread async prefetch
+// PF sweep (one-tile rows, M <= 2): every thread copies the cells it will own in
+// the NEXT item into its own slots of a double-buffered shared-memory slab with
+// cp.async (LDGSTS, no registers held while in flight), so an item's HBM reads
+// overlap the previous item's fp64 work.  Each thread reads back only what it
+// copied itself: cp.async.wait_group orders it, no barrier is needed.
+__device__ __forceinline__ unsigned pf_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(pf_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(pf_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// bytes of one item's slab per thread: x (M), y, v as double2; a2, a1, b2, b1 (M each) as CT[2]
+template <int M, typename CT>
+struct PFCfg {
+    static constexpr int XB16 = M + 2;                  // 16-byte chunks
+    static constexpr int CB = 2 * (int)sizeof(CT);      // bytes of one coefficient pair
+    static constexpr int PER_THREAD = 16 * XB16 + 4 * M * CB;
+};
+
+template <typename CT>
+__device__ __forceinline__ void cp_async_pair(void* dst, const CT* src) {
+    if constexpr (sizeof(CT) == 8) cp_async16(dst, src);
+    else cp_async8(dst, src);
+}
+template <typename CT>
+__device__ __forceinline__ void lds2(const unsigned char* p, double* o) {
+    if constexpr (sizeof(CT) == 8) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        o[0] = t.x;
+        o[1] = t.y;
+    } else {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        o[0] = (double)t.x;
+        o[1] = (double)t.y;
+    }
+}
+
+// issue this thread's copies of row jj (its cells kl, kl+1) into slab buffer buf
+template <int M, typename CT>
+__device__ __forceinline__ void pf_issue(const KArgs& a, unsigned char* buf, int bs, int tid,
+                                         long long jj, int kl, long long qn) {
+    using C = PFCfg<M, CT>;
+    const long long ro = jj * a.n_pad + kl;
+#pragma unroll
+    for (int i = 0; i < M; ++i) cp_async16(buf + ((size_t)i * bs + tid) * 16, a.x + i * qn + ro);
+    cp_async16(buf + ((size_t)M * bs + tid) * 16, a.y + ro);
+    cp_async16(buf + ((size_t)(M + 1) * bs + tid) * 16, a.v + ro);
+    unsigned char* cb = buf + (size_t)C::XB16 * bs * 16;
+    const CT* src[4];
+    if constexpr (sizeof(CT) == 4) {
+        src[0] = a.fa2; src[1] = a.fa1; src[2] = a.fb2; src[3] = a.fb1;
+    } else {
+        src[0] = reinterpret_cast<const CT*>(a.a2); src[1] = reinterpret_cast<const CT*>(a.a1);
+        src[2] = reinterpret_cast<const CT*>(a.b2); src[3] = reinterpret_cast<const CT*>(a.b1);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            cp_async_pair<CT>(cb + ((size_t)(4 * i + c) * bs + tid) * C::CB, src[c] + i * qn + ro);
+    cp_async_commit();
+}
+
 // ---------------------------------------------------------------- the sweep
 // Row finalisation for (i, j) (PAPER.md:432-448 via identity I1):
 //   W = sum_k (g(x_k) - lam) = Sg + sum_k b0 - n lam,  t = h + p - W,
@@ -517,8 +808,18 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
 // (an infinite bound): fp64 block reductions with barriers.
 // CT = float: F2 mixed precision -- a2, a1, b2, b1 read from their fp32 copies
 // (16 instead of 32 bytes per element), every operation in fp64.
-template <int M, int MODE, bool FX, typename CT>
-__global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
+// PF = true (one-tile rows, M <= 2, implies FX): cp.async prefetch of the next
+// item into a double-buffered dynamic shared-memory slab (see pf_issue).
+#ifndef SWEEP_LB
+#define SWEEP_LB 512
+#endif
+// U = cells (consecutive steps k) per thread: 2 (one double2 per stream) or 4
+// (two; four interleaved Gauss-Seidel chains per thread, 256-thread CTAs).
+template <int M, int MODE, bool FX, typename CT, bool PF, int U>
+__global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep_kernel(KArgs a) {
+    static_assert(!PF || FX, "the prefetching sweep is barrier-free (FX)");
+    static_assert(!PF || U == 2, "the prefetching sweep moves one double2 per stream");
+    static_assert(U == 2 || U == 4, "2 or 4 cells per thread");
     const long long it = *(volatile long long*)a.iter;
     const Ctrl& cin = a.ctrl[it & 1];
     if (cin.done || it >= a.prm->iter_limit) return;
@@ -571,59 +872,138 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
 #pragma unroll
     for (int i = 0; i < M; ++i) x1c[i] = cin.x1[i];
     const bool nu_pending = cin.nu_pending != 0;
+    extern __shared__ __align__(16) unsigned char pf_sm[];
+    const size_t pf_buf = (size_t)blockDim.x * PFCfg<M, CT>::PER_THREAD;
+    const int pf_kl = (U * tid < a.n_pad) ? U * tid : 0;  // T == 1: tile 0 only
+    double lam_nx[M], zeta_nx[M], nu_nx[M];                  // next row's scalars (PF)
+    if constexpr (PF) {
+        if (blockIdx.x < nitems) {
+            pf_issue<M, CT>(a, pf_sm, blockDim.x, tid, blockIdx.x, pf_kl, qn);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const long long rix = (long long)i * a.q + blockIdx.x;
+                lam_nx[i] = __ldcg(a.lam + rix);
+                zeta_nx[i] = __ldcg(a.zeta + rix);
+                nu_nx[i] = tid == 0 ? __ldcg(a.nu + rix) : 0.0;
+            }
+        }
+    }
     for (long long item = blockIdx.x; item < nitems; item += a.G, ++litem,
                    j += gT + ((tile += gR) >= a.T ? 1 : 0), tile -= (tile >= a.T ? a.T : 0)) {
-        const int k = tile * a.tile + CPT * tid;  // first of this thread's 2 cells
-        const bool inb = k < a.n_pad;             // n_pad % 4 == 0: both cells in bounds
-        const bool v0 = k < a.n, v1 = (k + 1) < a.n;
+        const int k = tile * a.tile + U * tid;  // first of this thread's U cells
+        const bool inb = k < a.n_pad;           // n_pad % 4 == 0: all U cells in bounds
+        bool vc[U];
+#pragma unroll
+        for (int c = 0; c < U; ++c) vc[c] = (k + c) < a.n;
         const int kl = inb ? k : 0;  // out-of-range threads load cell 0 (results discarded)
 
-        double xo[M][2], xn[M][2];
+        double xo[M][U], xn[M][U];
         double Sg[M], dgx[M], dgn[M];
-        double yv[2], vv[2];
-        {
-            const double2 t2 = __ldg(reinterpret_cast<const double2*>(a.y + j * a.n_pad + kl));
-            yv[0] = t2.x; yv[1] = t2.y;
-            const double2 u2 = *(reinterpret_cast<const double2*>(a.v + j * a.n_pad + kl));
-            vv[0] = u2.x; vv[1] = u2.y;
-        }
+        double yv[U], vv[U];
+        double ca2[M][U], ca1[M][U], cb2[M][U], cb1[M][U], clo[M][U], chi[M][U];
+        double lam_e[M], zeta_o[M], nu_e[M], nu_ld[M];
+        if constexpr (PF) {
+            // next item's copies go out first, then this item's (issued one item ago) land
+            const long long jn = j + a.G;
+            unsigned char* cur = pf_sm + (size_t)(litem & 1) * pf_buf;
+            if (jn < a.q) pf_issue<M, CT>(a, pf_sm + (size_t)((litem + 1) & 1) * pf_buf, blockDim.x, tid, jn,
+                                          pf_kl, qn);
+            else cp_async_commit();  // empty group: wait_group 1 below still means "this item"
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                lam_e[i] = lam_nx[i] * f[0];
+                zeta_o[i] = zeta_nx[i];
+                nu_ld[i] = nu_nx[i];
+            }
+            if (jn < a.q) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const long long rix = (long long)i * a.q + jn;
+                    lam_nx[i] = __ldcg(a.lam + rix);
+                    zeta_nx[i] = __ldcg(a.zeta + rix);
+                    nu_nx[i] = tid == 0 ? __ldcg(a.nu + rix) : 0.0;
+                }
+            }
+            cp_async_wait1();
+            const int bsz = blockDim.x;
+            lds2<double>(cur + ((size_t)M * bsz + tid) * 16, yv);
+            lds2<double>(cur + ((size_t)(M + 1) * bsz + tid) * 16, vv);
+            const unsigned char* cb = cur + (size_t)PFCfg<M, CT>::XB16 * bsz * 16;
+            constexpr int CB = PFCfg<M, CT>::CB;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                lds2<double>(cur + ((size_t)i * bsz + tid) * 16, xo[i]);
+                lds2<CT>(cb + ((size_t)(4 * i + 0) * bsz + tid) * CB, ca2[i]);
+                lds2<CT>(cb + ((size_t)(4 * i + 1) * bsz + tid) * CB, ca1[i]);
+                lds2<CT>(cb + ((size_t)(4 * i + 2) * bsz + tid) * CB, cb2[i]);
+                lds2<CT>(cb + ((size_t)(4 * i + 3) * bsz + tid) * CB, cb1[i]);
+                const long long bk = (long long)i * a.n_pad + kl;
+                double2 t;
+                t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
+                t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
+            }
+        } else if constexpr (U == 4) {
+            // staged: x, y, v into this thread's slab slots; coefficients read at use
+            double* slab = reinterpret_cast<double*>(pf_sm);
+            const int bsz = blockDim.x;
+            double t[4];
+            ldU<double, 4>(a.y + j * a.n_pad + kl, t);
+            wr4(slab + ((size_t)Slab4<M>::Y * bsz + tid) * 4, t);
+            ldvU<4>(a.v + j * a.n_pad + kl, t);
+            wr4(slab + ((size_t)Slab4<M>::V * bsz + tid) * 4, t);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                ldvU<4>(a.x + (long long)i * qn + j * a.n_pad + kl, t);
+                wr4(slab + ((size_t)(Slab4<M>::XO + i) * bsz + tid) * 4, t);
+                xo[i][0] = t[0];  // consensus cell (lazy (6h) below)
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const long long rix = (long long)i * a.q + j;
+                lam_e[i] = __ldcg(a.lam + rix) * f[0];
+                zeta_o[i] = __ldcg(a.zeta + rix);
+                nu_ld[i] = 0.0;
+            }
+        } else {
+        ldU<double, U>(a.y + j * a.n_pad + kl, yv);
+        ldvU<U>(a.v + j * a.n_pad + kl, vv);
         // coefficient streams, all issued up front
-        double ca2[M][2], ca1[M][2], cb2[M][2], cb1[M][2], clo[M][2], chi[M][2];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const long long e = (long long)i * qn + j * a.n_pad + kl;
-            double2 t;
-            t = *(reinterpret_cast<const double2*>(a.x + e));  xo[i][0] = t.x; xo[i][1] = t.y;
+            ldvU<U>(a.x + e, xo[i]);
             if constexpr (sizeof(CT) == 4) {
-                ld2<float>(a.fa2 + e, ca2[i]);
-                ld2<float>(a.fa1 + e, ca1[i]);
-                ld2<float>(a.fb2 + e, cb2[i]);
-                ld2<float>(a.fb1 + e, cb1[i]);
+                ldU<float, U>(a.fa2 + e, ca2[i]);
+                ldU<float, U>(a.fa1 + e, ca1[i]);
+                ldU<float, U>(a.fb2 + e, cb2[i]);
+                ldU<float, U>(a.fb1 + e, cb1[i]);
             } else {
-                ld2<double>(a.a2 + e, ca2[i]);
-                ld2<double>(a.a1 + e, ca1[i]);
-                ld2<double>(a.b2 + e, cb2[i]);
-                ld2<double>(a.b1 + e, cb1[i]);
+                ldU<double, U>(a.a2 + e, ca2[i]);
+                ldU<double, U>(a.a1 + e, ca1[i]);
+                ldU<double, U>(a.b2 + e, cb2[i]);
+                ldU<double, U>(a.b1 + e, cb1[i]);
             }
             const long long bk = (long long)i * a.n_pad + kl;
-            t = __ldg(reinterpret_cast<const double2*>(a.lo + bk)); clo[i][0] = t.x; clo[i][1] = t.y;
-            t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
+            ldU<double, U>(a.lo + bk, clo[i]);
+            ldU<double, U>(a.hi + bk, chi[i]);
         }
         // per-row scalars (uniform loads)
-        double lam_e[M], zeta_o[M], nu_e[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             const long long rix = (long long)i * a.q + j;
             lam_e[i] = __ldcg(a.lam + rix) * f[0];
             zeta_o[i] = __ldcg(a.zeta + rix);
-            nu_e[i] = 0.0;
+            nu_ld[i] = 0.0;
         }
+        }  // !PF loads
+#pragma unroll
+        for (int i = 0; i < M; ++i) nu_e[i] = 0.0;
         const bool owns_k0 = (k == 0);
         if (owns_k0) {
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 const long long rix = (long long)i * a.q + j;
-                double nu = __ldcg(a.nu + rix);
+                double nu = PF ? nu_ld[i] : __ldcg(a.nu + rix);
                 // lazy (6h) of the previous iteration, then its dual rescale
                 if (nu_pending) nu = nu + x1c[i] - xo[i][0];
                 nu_e[i] = nu * f[3];
@@ -638,21 +1018,48 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             zl[i] = zeta_o[i] + lam_e[i];
             x1nu[i] = x1c[i] + nu_e[i];
         }
-        double vn[2];
+        double vn[U];
         {
-            const double s_e[2] = {fmax(vv[0], 0.0), fmax(vv[1], 0.0)};
-            const double mu_e[2] = {vv[0] < 0.0 ? -vv[0] * f[2] : 0.0, vv[1] < 0.0 ? -vv[1] * f[2] : 0.0};
-            gs_cell2<M, MODE>(ca2, ca1, cb2, cb1, clo, chi, xo, xn, yv, s_e, mu_e, zl, rho, iq,
-                              owns_k0, x1nu);
+            if constexpr (U == 4) {
+                double* slab = reinterpret_cast<double*>(pf_sm);
+                const int bsz = blockDim.x;
+                staged_gs4<M, MODE, CT>(a, slab, bsz, tid, j * a.n_pad + kl, qn, kl, zl, rho, iq, owns_k0,
+                                        x1nu, f[2]);
+                // tail operands back into registers (live only from here on)
+                rd4(slab + ((size_t)Slab4<M>::Y * bsz + tid) * 4, yv);
+                rd4(slab + ((size_t)Slab4<M>::V * bsz + tid) * 4, vv);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
+                for (int i = 0; i < M; ++i) {
+                    rd4(slab + ((size_t)(Slab4<M>::XO + i) * bsz + tid) * 4, xo[i]);
+                    rd4(slab + ((size_t)(Slab4<M>::XN + i) * bsz + tid) * 4, xn[i]);
+                    const long long e = (long long)i * qn + j * a.n_pad + kl;
+                    if constexpr (sizeof(CT) == 4) {
+                        ldU<float, 4>(a.fb2 + e, cb2[i]);
+                        ldU<float, 4>(a.fb1 + e, cb1[i]);
+                    } else {
+                        ldU<double, 4>(a.b2 + e, cb2[i]);
+                        ldU<double, 4>(a.b1 + e, cb1[i]);
+                    }
+                }
+            } else {
+                double s_e[U], mu_e[U];
+#pragma unroll
+                for (int c = 0; c < U; ++c) {
+                    s_e[c] = fmax(vv[c], 0.0);
+                    mu_e[c] = vv[c] < 0.0 ? -vv[c] * f[2] : 0.0;
+                }
+                gs_cellU<M, MODE, U>(ca2, ca1, cb2, cb1, clo, chi, xo, xn, yv, s_e, mu_e, zl, rho, iq,
+                                     owns_k0, x1nu);
+            }
+#pragma unroll
+            for (int c = 0; c < U; ++c) {
                 double txo[M], txn[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     txo[i] = xo[i][c];
                     txn[i] = xn[i][c];
                 }
-                const bool valid = c == 0 ? v0 : v1;
+                const bool valid = vc[c];
                 double r1l = my_r1, s3l = my_s3;
                 const double vnew = cell_tail<M>(txo, txn, yv[c], vv[c], f[2], is_check && valid, r1l, s3l);
                 my_r1 = r1l;
@@ -666,8 +1073,8 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             dgx[i] = -INFINITY;
             dgn[i] = INFINITY;
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const bool valid = c == 0 ? v0 : v1;
+            for (int c = 0; c < U; ++c) {
+                const bool valid = vc[c];
                 if (!valid) xn[i][c] = 0.0;  // padding stays 0
                 if (valid) {
                     const double b2 = cb2[i][c], b1 = cb1[i][c];
@@ -681,12 +1088,9 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             }
         }
         if (inb) {
-            *(reinterpret_cast<double2*>(a.v + j * a.n_pad + k)) = make_double2(vn[0], vn[1]);
+            stU<U>(a.v + j * a.n_pad + k, vn);
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                const long long e = (long long)i * qn + j * a.n_pad + k;
-                *(reinterpret_cast<double2*>(a.x + e)) = make_double2(xn[i][0], xn[i][1]);
-            }
+            for (int i = 0; i < M; ++i) stU<U>(a.x + (long long)i * qn + j * a.n_pad + k, xn[i]);
         }
         if (owns_k0) {
 #pragma unroll
@@ -716,8 +1120,8 @@ __global__ void __launch_bounds__(512) sweep_kernel(KArgs a) {
             for (int i = 0; i < M; ++i) {
                 long long fx = 0;
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    if (c == 0 ? v0 : v1)
+                for (int c = 0; c < U; ++c)
+                    if (vc[c])
                         fx += __double2ll_rn(fma(cb2[i][c], xn[i][c], cb1[i][c]) * xn[i][c] * a.fx_scale[i]);
                 const unsigned long long ws = warp_sum_u64((unsigned long long)fx);
                 if (lane == 0) s_fxw[b][wid][i] = ws;

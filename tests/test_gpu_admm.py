@@ -50,28 +50,34 @@ def compare_states(P, So, Sg, tol=1e-9):
 # with a grid barrier per iteration (forced through ADMM_PERSIST_GRID=1); the
 # barrier-free fixed-point sweep on every shape (ADMM_SWEEP_FX=1) and the opt-in
 # TMA-pipelined sweep (ADMM_STREAM_TMA=1)
+# ... and the measured-but-not-default sweep variants: cp.async prefetch of the next
+# item (ADMM_SWEEP_PF=1) and four cells per thread staged through shared memory
+# (ADMM_SWEEP_CPT=4; created per solver, so set before AdmmSolver())
 ENGINES = ["stream", "cluster", "grid"]
-ALT_ENGINES = ["stream_fx", "stream_tma"]
-_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_fx": 1, "stream_tma": 1, 0: 0}
+ALT_ENGINES = ["stream_fx", "stream_tma", "stream_pf", "stream_u4"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_fx": 1, "stream_tma": 1, "stream_pf": 1,
+         "stream_u4": 1, 0: 0}
 _ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_fx": {"ADMM_SWEEP_FX": "1"},
-        "stream_tma": {"ADMM_STREAM_TMA": "1"}}
-_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA")
+        "stream_tma": {"ADMM_STREAM_TMA": "1"}, "stream_pf": {"ADMM_SWEEP_PF": "1"},
+        "stream_u4": {"ADMM_SWEEP_CPT": "4"}}
+_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA", "ADMM_SWEEP_PF",
+             "ADMM_SWEEP_CPT")
 
 
 def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_iter=None,
             engine=0):
     L = _lib()
+    import os
+
+    for k in _ENV_KEYS:
+        os.environ.pop(k, None)
+    os.environ.update(_ENV.get(engine, {}))
     s = L.AdmmSolver(P["m"], P["n"], P["q"], rho=params["rho0"], tau=params["tau"],
                      hi_ratio=params["hi_ratio"], lo_ratio=params["lo_ratio"],
                      r_bar=params["r_bar"], sigma_bar=params["sigma_bar"],
                      check_every=params["check_every"], adapt_rho=params["adapt_rho"],
                      rescale_duals=params["rescale_duals"], box_mode=params["box_mode"],
                      exec_mode=_EXEC[engine])
-    import os
-
-    for k in _ENV_KEYS:
-        os.environ.pop(k, None)
-    os.environ.update(_ENV.get(engine, {}))
     s.set_problem(P)
     info = None
     if mode == "iterate":
