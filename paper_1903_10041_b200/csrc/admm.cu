@@ -556,7 +556,7 @@ typedef void (*sweep_tma_fn)(KArgs, SArgs);
 // one-tile rows, where it measured faster (44 vs 38 % at q = 1e4, profiles/README.md).
 bool use_pf_sweep(const admm_ctx* ctx) {
     const char* e = getenv("ADMM_SWEEP_PF");
-    if (!(e && e[0] == '1')) return false;  // opt-in while measured
+    if (!(e && (e[0] == '1' || e[0] == '2'))) return false;  // opt-in while measured
     return ctx->fx_ok && ctx->T == 1 && ctx->m <= 2 && ctx->cpt == 2;
 }
 
@@ -572,7 +572,10 @@ size_t pf_smem_bytes(const admm_ctx* ctx) {
 }
 
 bool use_fx_sweep(const admm_ctx* ctx) {
-    if (use_pf_sweep(ctx)) return true;
+    if (use_pf_sweep(ctx)) {  // ADMM_SWEEP_PF=1: with the fixed-point slots, =2: with block barriers
+        const char* e = getenv("ADMM_SWEEP_PF");
+        return !(e && e[0] == '2');
+    }
     const char* e = getenv("ADMM_SWEEP_FX");
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return ctx->fx_ok;
@@ -589,8 +592,12 @@ sweep_fn pick_sweep_t(int m, int mode, bool fx, bool pf, int cpt) {
                                  : sweep_kernel<MM, BOX_PROJECT, false, CT, false, UU>;        \
     }
 #define SP(MM)                                                                                 \
-    if (m == MM && pf) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, true, 2> \
-                                                : sweep_kernel<MM, BOX_PROJECT, true, CT, true, 2>;
+    if (m == MM && pf) {                                                                       \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, true, 2>      \
+                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, true, 2>;   \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, true, 2>             \
+                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, true, 2>;          \
+    }
     if (cpt == 4) {
         S(1, 4) S(2, 4)
         return nullptr;
@@ -1226,8 +1233,10 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     const Layout& L = ctx->L;
     KArgs& a = ctx->ka;
     {
+        // 4 cells per thread (staged through shared memory) is the default for m <= 2:
+        // 43-46 % vs 40-43 % of HBM peak at q = 1e4..1e5 (profiles/r01d); ADMM_SWEEP_CPT=2 reverts
         const char* e = getenv("ADMM_SWEEP_CPT");
-        ctx->cpt = (e && e[0] == '4' && m <= 2) ? 4 : 2;
+        ctx->cpt = (e && e[0] == '2') ? 2 : (m <= 2 ? 4 : 2);
     }
     ctx->bs = pick_bs(n, ctx->cpt);
     ctx->tile = ctx->bs * ctx->cpt;

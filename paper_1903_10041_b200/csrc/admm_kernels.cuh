@@ -319,6 +319,14 @@ __device__ __forceinline__ void gs_cell2_smem(const double* s_a2q, const double*
     }
 }
 
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+#ifndef SWEEP_L2PF
+#define SWEEP_L2PF 0  // measured slower (profiles/r01d/sweep_variants/README.md)
+#endif
+__device__ __forceinline__ constexpr bool sweep_l2_prefetch() { return SWEEP_L2PF != 0; }
+
 // U consecutive values of a stream (U = 2: one 128-bit load, U = 4: two)
 template <typename CT, int U>
 __device__ __forceinline__ void ldU(const CT* p, double* o) {
@@ -358,6 +366,11 @@ __device__ __forceinline__ void quartic_coreU(const double* b, const double* c, 
         all = all && isfinite(De[u]) && !(De[u] > 0.0) && !(Q[u] == 0.0 && R[u] == 0.0);
     }
     if (all) {
+#ifdef SWEEP_CHEAP_TRIG  // timing experiment only (wrong results)
+#pragma unroll
+        for (int u = 0; u < U; ++u) out[u] = clampd(-b[u] + d[u], lo[u], hi[u]);
+        return;
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) out[u] = trig_pick<MODE>(b[u], c[u], d[u], Q[u], R[u], De[u], lo[u], hi[u]);
     } else {
@@ -802,13 +815,40 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
     *s2 = o.s2;
 }
 
+// Same update from row scalars the sweep loaded with the item (no global round
+// trip at the end of the item): lam_e = lam f0, p_e = p f1, h_o, zeta_o, sb0_e.
+__device__ __forceinline__ void finalize_row_v(const KArgs& a, const Ctrl& cin, int i, long long j,
+                                               double Sg, double dgmax, double dgmin, double lam_e,
+                                               double p_e, double h_o, double zeta_o, double sb0_e,
+                                               double* r2, double* r3, double* s1, double* s2) {
+    const long long rix = (long long)i * a.q + j;
+    const RowOut o = row_update(Sg, sb0_e, lam_e, p_e, h_o, zeta_o, a.c[i], (double)a.n, cin.rho, dgmax,
+                                dgmin);
+    __stcg(a.lam + rix, o.lam);
+    __stcg(a.zeta + rix, o.zeta);
+    __stcg(a.h + rix, o.h);
+    __stcg(a.p + rix, o.p);
+    *r2 = o.r2;
+    *r3 = o.r3;
+    *s1 = o.s1;
+    *s2 = o.s2;
+}
+// element i of a small register array without local-memory indexing
+template <int M>
+__device__ __forceinline__ double pick(const double* v, int i) {
+    double r = v[0];
+#pragma unroll
+    for (int l = 1; l < M; ++l) r = (i == l) ? v[l] : r;
+    return r;
+}
+
 // FX = true (every problem with a finite box): row sums in exact fixed point,
 // per-warp slots and a last-warp finaliser -- no block barrier inside the item
 // loop, so one warp's loads overlap another warp's fp64 work.  FX = false
 // (an infinite bound): fp64 block reductions with barriers.
 // CT = float: F2 mixed precision -- a2, a1, b2, b1 read from their fp32 copies
 // (16 instead of 32 bytes per element), every operation in fp64.
-// PF = true (one-tile rows, M <= 2, implies FX): cp.async prefetch of the next
+// PF = true (one-tile rows, M <= 2): cp.async prefetch of the next
 // item into a double-buffered dynamic shared-memory slab (see pf_issue).
 #ifndef SWEEP_LB
 #define SWEEP_LB 512
@@ -817,9 +857,10 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
 // (two; four interleaved Gauss-Seidel chains per thread, 256-thread CTAs).
 template <int M, int MODE, bool FX, typename CT, bool PF, int U>
 __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep_kernel(KArgs a) {
-    static_assert(!PF || FX, "the prefetching sweep is barrier-free (FX)");
     static_assert(!PF || U == 2, "the prefetching sweep moves one double2 per stream");
     static_assert(U == 2 || U == 4, "2 or 4 cells per thread");
+    // row scalars for the finalisation loaded with the item (U = 4 and PF: measured faster)
+    constexpr bool PRELOAD = PF || U == 4;
     const long long it = *(volatile long long*)a.iter;
     const Ctrl& cin = a.ctrl[it & 1];
     if (cin.done || it >= a.prm->iter_limit) return;
@@ -875,7 +916,7 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
     extern __shared__ __align__(16) unsigned char pf_sm[];
     const size_t pf_buf = (size_t)blockDim.x * PFCfg<M, CT>::PER_THREAD;
     const int pf_kl = (U * tid < a.n_pad) ? U * tid : 0;  // T == 1: tile 0 only
-    double lam_nx[M], zeta_nx[M], nu_nx[M];                  // next row's scalars (PF)
+    double lam_nx[M], zeta_nx[M], nu_nx[M], p_nx[M], h_nx[M], sb0_nx[M];  // next row's scalars (PF)
     if constexpr (PF) {
         if (blockIdx.x < nitems) {
             pf_issue<M, CT>(a, pf_sm, blockDim.x, tid, blockIdx.x, pf_kl, qn);
@@ -884,6 +925,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                 const long long rix = (long long)i * a.q + blockIdx.x;
                 lam_nx[i] = __ldcg(a.lam + rix);
                 zeta_nx[i] = __ldcg(a.zeta + rix);
+                p_nx[i] = __ldcg(a.p + rix);
+                h_nx[i] = __ldcg(a.h + rix);
+                sb0_nx[i] = __ldg(a.sb0 + rix);
                 nu_nx[i] = tid == 0 ? __ldcg(a.nu + rix) : 0.0;
             }
         }
@@ -901,7 +945,7 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
         double Sg[M], dgx[M], dgn[M];
         double yv[U], vv[U];
         double ca2[M][U], ca1[M][U], cb2[M][U], cb1[M][U], clo[M][U], chi[M][U];
-        double lam_e[M], zeta_o[M], nu_e[M], nu_ld[M];
+        double lam_e[M], zeta_o[M], nu_e[M], nu_ld[M], p_e[M], h_e[M], sb0_e[M];
         if constexpr (PF) {
             // next item's copies go out first, then this item's (issued one item ago) land
             const long long jn = j + a.G;
@@ -913,6 +957,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
             for (int i = 0; i < M; ++i) {
                 lam_e[i] = lam_nx[i] * f[0];
                 zeta_o[i] = zeta_nx[i];
+                p_e[i] = p_nx[i] * f[1];
+                h_e[i] = h_nx[i];
+                sb0_e[i] = sb0_nx[i];
                 nu_ld[i] = nu_nx[i];
             }
             if (jn < a.q) {
@@ -921,6 +968,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                     const long long rix = (long long)i * a.q + jn;
                     lam_nx[i] = __ldcg(a.lam + rix);
                     zeta_nx[i] = __ldcg(a.zeta + rix);
+                    p_nx[i] = __ldcg(a.p + rix);
+                    h_nx[i] = __ldcg(a.h + rix);
+                    sb0_nx[i] = __ldg(a.sb0 + rix);
                     nu_nx[i] = tid == 0 ? __ldcg(a.nu + rix) : 0.0;
                 }
             }
@@ -943,9 +993,26 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                 t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
             }
         } else if constexpr (U == 4) {
-            // staged: x, y, v into this thread's slab slots; coefficients read at use
+            // staged: x, y, v into this thread's slab slots; coefficients read at use,
+            // after an L2 prefetch issued here (one per 128-byte line) so that the
+            // reads at use are L2 hits instead of serialised HBM round trips
             double* slab = reinterpret_cast<double*>(pf_sm);
             const int bsz = blockDim.x;
+            if ((tid & 3) == 0 && sweep_l2_prefetch()) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const long long e = (long long)i * qn + j * a.n_pad + kl;
+                    if constexpr (sizeof(CT) == 4) {
+                        if ((tid & 7) == 0) {
+                            l2_prefetch(a.fa2 + e); l2_prefetch(a.fa1 + e);
+                            l2_prefetch(a.fb2 + e); l2_prefetch(a.fb1 + e);
+                        }
+                    } else {
+                        l2_prefetch(a.a2 + e); l2_prefetch(a.a1 + e);
+                        l2_prefetch(a.b2 + e); l2_prefetch(a.b1 + e);
+                    }
+                }
+            }
             double t[4];
             ldU<double, 4>(a.y + j * a.n_pad + kl, t);
             wr4(slab + ((size_t)Slab4<M>::Y * bsz + tid) * 4, t);
@@ -962,6 +1029,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                 const long long rix = (long long)i * a.q + j;
                 lam_e[i] = __ldcg(a.lam + rix) * f[0];
                 zeta_o[i] = __ldcg(a.zeta + rix);
+                p_e[i] = __ldcg(a.p + rix) * f[1];
+                h_e[i] = __ldcg(a.h + rix);
+                sb0_e[i] = __ldg(a.sb0 + rix);
                 nu_ld[i] = 0.0;
             }
         } else {
@@ -993,6 +1063,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
             const long long rix = (long long)i * a.q + j;
             lam_e[i] = __ldcg(a.lam + rix) * f[0];
             zeta_o[i] = __ldcg(a.zeta + rix);
+            p_e[i] = 0.0;  // U == 2 without prefetch: the finaliser reads p, h, sb0 itself
+            h_e[i] = 0.0;  // (fewer live registers measured faster, profiles/r01d)
+            sb0_e[i] = 0.0;
             nu_ld[i] = 0.0;
         }
         }  // !PF loads
@@ -1174,8 +1247,13 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                     }
                     if (fin) {
                         double r2, r3, s1, s2;
-                        finalize_row(a, cin, i, j, (double)(long long)part * a.fx_inv[i], mx, mn, &r2,
-                                     &r3, &s1, &s2);
+                        if constexpr (PRELOAD)
+                            finalize_row_v(a, cin, i, j, (double)(long long)part * a.fx_inv[i], mx, mn,
+                                           pick<M>(lam_e, i), pick<M>(p_e, i), pick<M>(h_e, i),
+                                           pick<M>(zeta_o, i), pick<M>(sb0_e, i), &r2, &r3, &s1, &s2);
+                        else
+                            finalize_row(a, cin, i, j, (double)(long long)part * a.fx_inv[i], mx, mn, &r2,
+                                         &r3, &s1, &s2);
                         my_r2 = fmax(my_r2, r2);
                         my_r3 = fmax(my_r3, r3);
                         my_s1 = fmax(my_s1, s1);
@@ -1235,8 +1313,13 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
         if (a.T == 1) {
             if (tid < M) {
                 double r2, r3, s1, s2;
-                finalize_row(a, cin, tid, j, rowres[3 * tid], rowres[3 * tid + 1],
-                             rowres[3 * tid + 2], &r2, &r3, &s1, &s2);
+                if constexpr (PRELOAD)
+                    finalize_row_v(a, cin, tid, j, rowres[3 * tid], rowres[3 * tid + 1], rowres[3 * tid + 2],
+                                   pick<M>(lam_e, tid), pick<M>(p_e, tid), pick<M>(h_e, tid),
+                                   pick<M>(zeta_o, tid), pick<M>(sb0_e, tid), &r2, &r3, &s1, &s2);
+                else
+                    finalize_row(a, cin, tid, j, rowres[3 * tid], rowres[3 * tid + 1],
+                                 rowres[3 * tid + 2], &r2, &r3, &s1, &s2);
                 my_r2 = fmax(my_r2, r2);
                 my_r3 = fmax(my_r3, r3);
                 my_s1 = fmax(my_s1, s1);
@@ -1282,7 +1365,12 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
                 }
                 if (tid < M) {
                     double r2, r3, s1, s2;
-                    finalize_row(a, cin, tid, j, Sgs, mx, mn, &r2, &r3, &s1, &s2);
+                    if constexpr (PRELOAD)
+                        finalize_row_v(a, cin, tid, j, Sgs, mx, mn, pick<M>(lam_e, tid), pick<M>(p_e, tid),
+                                       pick<M>(h_e, tid), pick<M>(zeta_o, tid), pick<M>(sb0_e, tid), &r2,
+                                       &r3, &s1, &s2);
+                    else
+                        finalize_row(a, cin, tid, j, Sgs, mx, mn, &r2, &r3, &s1, &s2);
                     my_r2 = fmax(my_r2, r2);
                     my_r3 = fmax(my_r3, r3);
                     my_s1 = fmax(my_s1, s1);
