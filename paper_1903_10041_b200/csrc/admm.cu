@@ -488,6 +488,7 @@ struct admm_ctx {
     bool use_tma = false;         // streaming engine: TMA-pipelined sweep (else legacy sweep)
     int coeff_bits = 64;          // F2: storage precision of a2, a1, b2, b1 (64 or 32)
     int cpt = 2;                  // streaming sweep: cells per thread (2, or 4 for m <= 2)
+    int rl = 0;                   // streaming sweep: row loop, CTA size (0 = off, 128 or 64)
     bool graph_dirty = true;      // problem changed since the graph was captured
     SArgs sa{};
 };
@@ -583,20 +584,31 @@ bool use_fx_sweep(const admm_ctx* ctx) {
 }
 
 template <typename CT>
-sweep_fn pick_sweep_t(int m, int mode, bool fx, bool pf, int cpt) {
+sweep_fn pick_sweep_t(int m, int mode, bool fx, bool pf, int cpt, int rl) {
 #define S(MM, UU)                                                                              \
     if (m == MM) {                                                                             \
-        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, false, UU>    \
-                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, false, UU>; \
-        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, false, UU>           \
-                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, false, UU>;        \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, false, UU, 0> \
+                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, false, UU, 0>; \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, false, UU, 0>    \
+                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, false, UU, 0>; \
+    }
+#define SR(MM, TT)                                                                             \
+    if (m == MM) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, false, 2, TT> \
+                                          : sweep_kernel<MM, BOX_PROJECT, false, CT, false, 2, TT>;
+    if (rl == 128) {  // row loop: 128-thread CTAs own whole rows
+        SR(1, 128) SR(2, 128)
+        return nullptr;
+    }
+    if (rl == 64) {
+        SR(1, 64) SR(2, 64)
+        return nullptr;
     }
 #define SP(MM)                                                                                 \
     if (m == MM && pf) {                                                                       \
-        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, true, 2>      \
-                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, true, 2>;   \
-        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, true, 2>             \
-                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, true, 2>;          \
+        if (fx) return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, true, CT, true, 2, 0> \
+                                         : sweep_kernel<MM, BOX_PROJECT, true, CT, true, 2, 0>; \
+        return mode == BOX_EXACT ? sweep_kernel<MM, BOX_EXACT, false, CT, true, 2, 0>      \
+                                 : sweep_kernel<MM, BOX_PROJECT, false, CT, true, 2, 0>;   \
     }
     if (cpt == 4) {
         S(1, 4) S(2, 4)
@@ -606,13 +618,14 @@ sweep_fn pick_sweep_t(int m, int mode, bool fx, bool pf, int cpt) {
     S(1, 2) S(2, 2) S(3, 2) S(4, 2)
 #undef S
 #undef SP
+#undef SR
     return nullptr;
 }
 
 // f32: F2 mixed-precision sweep (coefficients read from their fp32 copies); pf: the
 // cp.async-prefetching sweep (one-tile rows, m <= 2; use_pf_sweep); cpt: cells per thread
-sweep_fn pick_sweep(int m, int mode, bool fx, bool f32, bool pf, int cpt) {
-    return f32 ? pick_sweep_t<float>(m, mode, fx, pf, cpt) : pick_sweep_t<double>(m, mode, fx, pf, cpt);
+sweep_fn pick_sweep(int m, int mode, bool fx, bool f32, bool pf, int cpt, int rl) {
+    return f32 ? pick_sweep_t<float>(m, mode, fx, pf, cpt, rl) : pick_sweep_t<double>(m, mode, fx, pf, cpt, rl);
 }
 
 // The prefetching sweep: rows of one tile (n <= 2 * block size), m <= 2, fixed-point
@@ -717,7 +730,7 @@ admm_status build_graph(admm_ctx* ctx) {
         cudaGraphDestroy(ctx->graph);
         ctx->graph = nullptr;
     }
-    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt);
+    sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt, ctx->rl);
     if (!fn) return fail(ctx, ADMM_ERR_INVALID, "m must be in 1..4");
     int occ = 0;
     const size_t dsm = pf_smem_bytes(ctx);
@@ -725,7 +738,7 @@ admm_status build_graph(admm_ctx* ctx) {
         CKC(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, ctx->bs, dsm));
     occ = std::max(1, std::min(occ, 32));
-    const long long items = ctx->q * ctx->T;
+    const long long items = ctx->rl ? ctx->q : ctx->q * ctx->T;
     ctx->G = (int)std::max(1LL, std::min(items, (long long)occ * ctx->sms));
     ctx->ka.G = ctx->G;
     {
@@ -1014,7 +1027,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         if (st != ADMM_OK) return st;
     } else if (ctx->no_graph) {
         // profiling mode (ADMM_NO_GRAPH=1): plain launches, host polls per body
-        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt);
+        sweep_fn fn = pick_sweep(ctx->m, ctx->params.box_mode, use_fx_sweep(ctx), ctx->coeff_bits == 32, use_pf_sweep(ctx), ctx->cpt, ctx->rl);
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
@@ -1237,8 +1250,15 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
         // 43-46 % vs 40-43 % of HBM peak at q = 1e4..1e5 (profiles/r01d); ADMM_SWEEP_CPT=2 reverts
         const char* e = getenv("ADMM_SWEEP_CPT");
         ctx->cpt = (e && e[0] == '2') ? 2 : (m <= 2 ? 4 : 2);
+        // row loop (128-thread CTAs own whole rows; 4 per SM): the default for m <= 2 when
+        // there are rows for every CTA (q >= 4 x SMs): q = 1e4 / 1e5 at 54 / 56 % of the
+        // HBM peak vs 44 / 46 % (profiles/r01e).  ADMM_SWEEP_RL = 0 off, 1 force, 6 = 64 threads
+        const char* r = getenv("ADMM_SWEEP_RL");
+        if (r) ctx->rl = (m <= 2) ? (r[0] == '1' ? 128 : (r[0] == '6' ? 64 : 0)) : 0;
+        else ctx->rl = (m <= 2 && ctx->q >= 4LL * ctx->sms) ? 128 : 0;
+        if (ctx->rl) ctx->cpt = 2;
     }
-    ctx->bs = pick_bs(n, ctx->cpt);
+    ctx->bs = ctx->rl ? (int)std::min<long long>(ctx->rl, ((n + 1) / 2 + 31) / 32 * 32) : pick_bs(n, ctx->cpt);
     ctx->tile = ctx->bs * ctx->cpt;
     ctx->T = (int)((n + ctx->tile - 1) / ctx->tile);
     a.m = m;

@@ -855,8 +855,17 @@ __device__ __forceinline__ double pick(const double* v, int i) {
 #endif
 // U = cells (consecutive steps k) per thread: 2 (one double2 per stream) or 4
 // (two; four interleaved Gauss-Seidel chains per thread, 256-thread CTAs).
-template <int M, int MODE, bool FX, typename CT, bool PF, int U>
-__global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep_kernel(KArgs a) {
+// RL = true (row loop, U = 2, block-barrier reductions): small CTAs (128 threads,
+// four per SM) each own whole rows and walk the row's tiles in order, keeping the
+// row partials in the finalising threads' registers -- no cross-CTA row reduction,
+// and four independent CTAs per SM overlap each other's load, compute and barrier
+// phases (tools/stream_probe.cu: this structure moves 89-92 % of the HBM peak with
+// no arithmetic, one 512-thread CTA per SM 70-73 %).
+template <int M, int MODE, bool FX, typename CT, bool PF, int U, int RLT>
+__global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? 512 / (RLT ? RLT : 1) : (U == 2 ? 1 : 2))
+    sweep_kernel(KArgs a) {
+    constexpr bool RL = RLT != 0;  // row loop with RLT-thread CTAs
+    static_assert(!RL || (U == 2 && !FX && !PF), "row loop: two-cell barrier variant only");
     static_assert(!PF || U == 2, "the prefetching sweep moves one double2 per stream");
     static_assert(U == 2 || U == 4, "2 or 4 cells per thread");
     // row scalars for the finalisation loaded with the item (U = 4 and PF: measured faster)
@@ -906,8 +915,17 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
     if (FX) __syncthreads();  // slot counters initialised
     long long litem = 0;
     // (row, tile) of the item, advanced incrementally (no 64-bit division per item)
-    long long j = (long long)blockIdx.x / a.T;
-    int tile = (int)((long long)blockIdx.x - j * a.T);
+    long long j = RL ? (long long)blockIdx.x : (long long)blockIdx.x / a.T;
+    int tile = RL ? 0 : (int)((long long)blockIdx.x - j * a.T);
+    // RL with multi-tile rows: per-thread row partials carried across the row's tiles,
+    // one block reduction per row (at its last tile)
+    double rt_S[M], rt_x[M], rt_n[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        rt_S[i] = 0.0;
+        rt_x[i] = -INFINITY;
+        rt_n[i] = INFINITY;
+    }
     const int gT = a.G / a.T, gR = a.G - gT * a.T;  // G = gT * T + gR
     double x1c[M];
 #pragma unroll
@@ -932,8 +950,9 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
             }
         }
     }
-    for (long long item = blockIdx.x; item < nitems; item += a.G, ++litem,
-                   j += gT + ((tile += gR) >= a.T ? 1 : 0), tile -= (tile >= a.T ? a.T : 0)) {
+    for (long long item = blockIdx.x; RL ? (j < a.q) : (item < nitems); item += a.G, ++litem,
+                   j += RL ? ((++tile == a.T) ? a.G : 0) : gT + ((tile += gR) >= a.T ? 1 : 0),
+                   tile -= (tile >= a.T ? a.T : 0)) {
         const int k = tile * a.tile + U * tid;  // first of this thread's U cells
         const bool inb = k < a.n_pad;           // n_pad % 4 == 0: all U cells in bounds
         bool vc[U];
@@ -1269,6 +1288,34 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
             }
             continue;
         }
+        if constexpr (RL) {
+            if (a.T > 1) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    rt_S[i] += Sg[i];
+                    rt_x[i] = fmax(rt_x[i], dgx[i]);
+                    rt_n[i] = fmin(rt_n[i], dgn[i]);
+                }
+                if (owns_k0) {  // (6c) contribution of k = 0 (thread 0, row order)
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        acc[i] += xn[i][0] - nu_e[i];
+                        acc[MAXM + i] = fmax(acc[MAXM + i], xn[i][0]);
+                        acc[2 * MAXM + i] = fmin(acc[2 * MAXM + i], xn[i][0]);
+                    }
+                }
+                if (tile < a.T - 1) continue;  // row not finished: no reduction yet
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    Sg[i] = rt_S[i];
+                    dgx[i] = rt_x[i];
+                    dgn[i] = rt_n[i];
+                    rt_S[i] = 0.0;
+                    rt_x[i] = -INFINITY;
+                    rt_n[i] = INFINITY;
+                }
+            }
+        }
         // ---- deterministic block reduction of Sg (sum), dg (max/min) per source
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -1310,7 +1357,17 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
         __syncthreads();
 
         // ---- row finalisation (6b),(6g),(6d),(6i)
-        if (a.T == 1) {
+        if (RL && a.T > 1) {  // this CTA owns every tile of the row (last tile here)
+            if (tid < M) {
+                double r2, r3, s1, s2;
+                finalize_row(a, cin, tid, j, rowres[3 * tid], rowres[3 * tid + 1], rowres[3 * tid + 2],
+                             &r2, &r3, &s1, &s2);
+                my_r2 = fmax(my_r2, r2);
+                my_r3 = fmax(my_r3, r3);
+                my_s1 = fmax(my_s1, s1);
+                my_s2 = fmax(my_s2, s2);
+            }
+        } else if (a.T == 1) {
             if (tid < M) {
                 double r2, r3, s1, s2;
                 if constexpr (PRELOAD)
@@ -1380,7 +1437,7 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
             }
         }
         // ---- (6c) consensus contributions of k = 0, in this CTA's item order
-        if (tile == 0 && tid < M) {
+        if (tile == 0 && tid < M && !(RL && a.T > 1)) {
             acc[tid] += k0x[tid] - k0nu[tid];
             acc[MAXM + tid] = fmax(acc[MAXM + tid], k0x[tid]);
             acc[2 * MAXM + tid] = fmin(acc[2 * MAXM + tid], k0x[tid]);
@@ -1443,11 +1500,24 @@ __global__ void __launch_bounds__(U == 2 ? SWEEP_LB : 256, U == 2 ? 1 : 2) sweep
         const bool is_sum = s < MAXM;
         const bool is_min = s >= 2 * MAXM && s < 3 * MAXM;
         const double ident = is_sum ? 0.0 : (is_min ? INFINITY : (s >= 3 * MAXM ? 0.0 : -INFINITY));
-        double v = ident;
-        for (int g = wid; g < a.G; g += nw) {
-            const double t = __ldcg(a.cta_part + (size_t)g * XB + s);
-            v = is_sum ? v + t : (is_min ? fmin(v, t) : fmax(v, t));
+        // eight independent accumulators per lane (loads in flight together: with
+        // 592 small CTAs a serial chain cost ~50 us per launch), combined in a fixed order
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vv[u] = ident;
+        for (int g0 = wid; g0 < a.G; g0 += 8 * nw) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int g = g0 + u * nw;
+                t[u] = g < a.G ? __ldcg(a.cta_part + (size_t)g * XB + s) : ident;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) vv[u] = is_sum ? vv[u] + t[u] : (is_min ? fmin(vv[u], t[u]) : fmax(vv[u], t[u]));
         }
+        double v = vv[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) v = is_sum ? v + vv[u] : (is_min ? fmin(v, vv[u]) : fmax(v, vv[u]));
         __shared__ double wred[16][XB];
         wred[wid][s] = v;
         __syncthreads();
