@@ -1354,7 +1354,9 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? 5
             }
         }
         __syncwarp();
-        __syncthreads();
+        // RL: rowres is produced and consumed by warp 0 only (the finalising threads
+        // are tid < M), so the other warps go on to the next row without a second barrier
+        if (!(RL && a.T > 1)) __syncthreads();
 
         // ---- row finalisation (6b),(6g),(6d),(6i)
         if (RL && a.T > 1) {  // this CTA owns every tile of the row (last tile here)
@@ -1443,7 +1445,10 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? 5
             acc[2 * MAXM + tid] = fmin(acc[2 * MAXM + tid], k0x[tid]);
         }
         __syncwarp();
-        __syncthreads();  // red/rowres/k0x reused by the next item
+        // red/rowres/k0x reused by the next item.  RL: red is read by warp 0 before it
+        // reaches the next reduction's barrier, rowres stays within warp 0, and k0x is
+        // not used (thread 0 adds the consensus term itself), so no barrier is needed
+        if (!(RL && a.T > 1)) __syncthreads();
     }
 
     // ---- per-CTA partials: block max of r1, s3 and of the row terms (held by the
