@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
-                    help="skip the q=1e4 streaming-sweep line added to the default phev run")
+                    help="skip the q=1e4 / 1e5 streaming-sweep lines added to the default phev run")
     return ap.parse_args()
 
 
@@ -282,7 +282,8 @@ def run_ours(args, rank, world, local_rank):
     achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if hbm else "fallback 6.65 TB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(args.workload, kname),
+            "frac": achieved / peak,
+            "traffic": ncu_traffic(f"{args.workload}_q{q_loc}", kname) or ncu_traffic(args.workload, kname),
             "alg_bytes_per_launch": per_launch, "alg_bytes_per_iteration": ab,
             "avg_launch_ms": avg_launch_ms, "note": note}
     res = dict(value=value, it_per_s=it_per_s, T=T, iters=iters, step_ms=step_ms,
@@ -613,13 +614,16 @@ def main():
         # HBM-streaming regime (configs[3] scenario sweep at q = 1e4), measured the same way
         import argparse as _ap
 
-        a2 = _ap.Namespace(**vars(args))
-        a2.workload, a2.q, a2.steps, a2.warmup, a2.no_e2e = "sweep", 10000, 3, 3, True
-        r2 = run_ours(a2, 0, 1, local_rank)
-        line["secondary"] = [{
-            "workload": r2["W"]["name"], "value": r2["value"], "unit": "element-updates/s",
-            "iterations_per_s": r2["it_per_s"], "ms_per_step": r2["T"] * 1e3 / a2.steps,
-            "engine": r2.get("engine"), "roofline": r2["roof"], "gpu_launches": r2["gpu_launches"]}]
+        line["secondary"] = []
+        for qs in (10000, 100000):
+            a2 = _ap.Namespace(**vars(args))
+            a2.workload, a2.q, a2.steps, a2.warmup, a2.no_e2e = "sweep", qs, 3, 3, True
+            r2 = run_ours(a2, 0, 1, local_rank)
+            line["secondary"].append({
+                "workload": r2["W"]["name"], "value": r2["value"], "unit": "element-updates/s",
+                "iterations_per_s": r2["it_per_s"], "ms_per_step": r2["T"] * 1e3 / a2.steps,
+                "engine": r2.get("engine"), "roofline": r2["roof"], "gpu_launches": r2["gpu_launches"],
+                "clocks": r2.get("clocks")})
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, sample, dt = oracle_rate(args, W)
         line["cpu_baseline"] = {"value": v, "unit": unit, "cores": 1, "kind": "oracle",
