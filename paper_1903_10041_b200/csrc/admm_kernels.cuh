@@ -4,8 +4,11 @@
 //
 // One kernel launch = one ADMM iteration ("sweep"):
 //   * a persistent grid of G CTAs walks work items (scenario j, horizon tile)
-//     in a fixed round-robin order (static => deterministic);
-//   * each thread owns CPT = 2 consecutive steps k of one scenario (128-bit
+//     in a fixed round-robin order (static => deterministic); three layouts
+//     (DESIGN.md §6): the row loop (RLT = 128: small CTAs, four per SM, each
+//     owning whole rows -- the default for m <= 2 with many rows), the staged
+//     four-cell CTA (U = 4) and the two-cell 512-thread CTA (m > 2);
+//   * each thread owns U = 2 (or 4) consecutive steps k of one scenario (128-bit
 //     double2 loads/stores of every SoA stream) and runs the Gauss-Seidel loop
 //     over sources i in registers: build the (6a) quartic, Algorithm 1, box;
 //   * (6e)/(6f) per cell in-thread (reduced state v = s - mu, identity I2);
@@ -178,60 +181,6 @@ __device__ __forceinline__ void gs_cell(const double* ca2, const double* ca1, co
     }
 }
 
-// (6a) for two cells of the same thread with interleaved Gauss-Seidel chains:
-// source i of both cells is built, then minimised together (quartic_core2:
-// straight-line trig evaluations that the scheduler interleaves), so the two
-// dependency chains overlap (ILP 2).  Same arithmetic as two gs_cell calls.
-// Arrays are [M][2] (cell index last); k0 marks cell 0 as the consensus cell.
-template <int M, int MODE>
-__device__ __forceinline__ void gs_cell2(const double (*ca2)[2], const double (*ca1)[2],
-                                         const double (*cb2)[2], const double (*cb1)[2],
-                                         const double (*clo)[2], const double (*chi)[2],
-                                         const double (*xo)[2], double (*xn)[2], const double* y,
-                                         const double* s_e, const double* mu_e, const double* zl,
-                                         const double* rho, double iq, bool k0, const double* x1nu) {
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double C[2], D[2], bn[2], cn[2], dn[2], lo[2], hi[2];
-        bool quart[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            double others = 0.0;
-#pragma unroll
-            for (int l = 0; l < M; ++l)
-                if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
-            const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
-            const double xoi = xo[i][u];
-            const double b2 = cb2[i][u], b1 = cb1[i][u];
-            const double e = fma(fma(b2, xoi, b1), xoi, zl[i]);
-            C[u] = fma(0.5 * rho[0], fma(b1, b1, -2.0 * b2 * e), fma(ca2[i][u], iq, 0.5 * rho[2]));
-            D[u] = fma(-rho[0] * b1, e, fma(ca1[i][u], iq, -rho[2] * phi));
-            if (k0 && u == 0) {
-                C[u] += 0.5 * rho[3];
-                D[u] += -rho[3] * x1nu[i];
-            }
-            quart[u] = (b2 != 0.0);
-            const double ia2 = rcp_nr(quart[u] ? rho[0] * b2 * b2 : 1.0);  // 1 / 2A
-            bn[u] = 1.5 * (rho[0] * b2 * b1) * ia2;
-            cn[u] = C[u] * ia2;
-            dn[u] = 0.5 * D[u] * ia2;
-            lo[u] = clo[i][u];
-            hi[u] = chi[i][u];
-        }
-        if (quart[0] && quart[1]) {
-            double r[2];
-            quartic_core2<MODE>(bn, cn, dn, C, D, lo, hi, r);
-            xn[i][0] = r[0];
-            xn[i][1] = r[1];
-        } else {
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-                xn[i][u] = quart[u] ? quartic_core<MODE>(bn[u], cn[u], dn[u], C[u], D[u], lo[u], hi[u])
-                                    : clampd(-D[u] * rcp_nr(2.0 * C[u]), lo[u], hi[u]);
-        }
-    }
-}
-
 // Same update from per-element constants prepared once per problem (on-chip
 // engines): a2q = a2/q, a1q = a1/q, bq = 1.5 b1/b2 (= b, independent of rho),
 // ib2s = 1/b2^2 (0 when b2 = 0).  R = {rho1, rho3, rho4, 1/rho1}.
@@ -379,7 +328,10 @@ __device__ __forceinline__ void quartic_coreU(const double* b, const double* c, 
     }
 }
 
-// gs_cell2 on U cells (arrays [M][U]); k0 marks cell 0 as the consensus cell
+// (6a) for U cells of one thread (arrays [M][U], cell index last): source i of all
+// U cells is built, then minimised together (quartic_coreU: straight-line trig
+// evaluations that the scheduler interleaves); same arithmetic as U gs_cell calls.
+// k0 marks cell 0 as the consensus cell.
 template <int M, int MODE, int U>
 __device__ __forceinline__ void gs_cellU(const double (*ca2)[U], const double (*ca1)[U],
                                          const double (*cb2)[U], const double (*cb1)[U],
@@ -862,7 +814,10 @@ __device__ __forceinline__ double pick(const double* v, int i) {
 // phases (tools/stream_probe.cu: this structure moves 89-92 % of the HBM peak with
 // no arithmetic, one 512-thread CTA per SM 70-73 %).
 template <int M, int MODE, bool FX, typename CT, bool PF, int U, int RLT>
-__global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? 512 / (RLT ? RLT : 1) : (U == 2 ? 1 : 2))
+#ifndef SWEEP_RL_MINB
+#define SWEEP_RL_MINB 4
+#endif
+__global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (RLT == 128 ? SWEEP_RL_MINB : 512 / (RLT ? RLT : 1)) : (U == 2 ? 1 : 2))
     sweep_kernel(KArgs a) {
     constexpr bool RL = RLT != 0;  // row loop with RLT-thread CTAs
     static_assert(!RL || (U == 2 && !FX && !PF), "row loop: two-cell barrier variant only");
