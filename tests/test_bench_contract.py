@@ -1,0 +1,59 @@
+"""bench.py host logic without a GPU: the algorithmic byte model (DESIGN.md "Byte
+model") and the reference arm's JSON contract."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    return bench
+
+
+def test_byte_model_fp64_matches_survey():
+    b = _bench()
+    m, n, q = 2, 1000, 50
+    # per element a2 a1 b2 b1 (32) + x r/w (16); per cell y + v r/w (24 / m); lo, hi per (i,k)
+    # shared by q scenarios; ~11 row scalars per (i,j)
+    per_elem = b.alg_bytes_per_iter(m, n, q) / (m * n * q)
+    assert abs(per_elem - (32 + 16 + 24 / m + 16 / q + 88 / n)) < 1e-12
+    assert 60.3 < per_elem < 60.5  # 60.3 B at m = 2, q >= 50
+
+
+def test_byte_model_f2_fp32_coefficients():
+    b = _bench()
+    m, n, q = 2, 1000, 100000
+    f64 = b.alg_bytes_per_iter(m, n, q, 64)
+    f32 = b.alg_bytes_per_iter(m, n, q, 32)
+    assert f64 - f32 == 16 * m * n * q  # four coefficient streams at 4 instead of 8 bytes
+    assert abs(f32 / (m * n * q) - 44.0) < 0.1
+
+
+def test_byte_model_horizon_m4():
+    b = _bench()
+    per_elem = b.alg_bytes_per_iter(4, 10**6, 1) / (4 * 10**6)
+    assert 69.9 < per_elem < 70.1  # 70 B at m = 4, q = 1
+
+
+def test_reference_arm_prints_one_json_line():
+    """--impl reference times the CPU oracle (the reference arm of this tier): one
+    JSON line with impl=reference, the same metric/unit as our arm, e2e and
+    cpu_baseline; no GPU needed."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--workload", "toy", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, cwd=ROOT, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["unit"] == "element-updates/s" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
