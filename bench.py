@@ -49,6 +49,8 @@ def parse():
                     help="microbench quartic family: C = convex (BASELINE.json configs[4]) or R")
     ap.add_argument("--coeff-bits", type=int, default=64, choices=[64, 32],
                     help="F2: storage precision of a2,a1,b2,b1 (32 = fp32 coefficients, fp64 math)")
+    ap.add_argument("--exec", type=int, default=0, choices=[0, 1, 2],
+                    help="admm_exec_mode: 0 auto (default), 1 streaming, 2 persistent")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true",
@@ -211,7 +213,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist = L.make_dist(q_total)
     s = L.AdmmSolver(m, n, q_total, device=local_rank, dist=dist, r_bar=W["r_bar"],
-                     sigma_bar=W["sigma_bar"], coeff_bits=args.coeff_bits)
+                     sigma_bar=W["sigma_bar"], coeff_bits=args.coeff_bits, exec_mode=args.exec)
     s.set_problem(P)
 
     def step():
