@@ -268,14 +268,6 @@ __device__ __forceinline__ void gs_cell2_smem(const double* s_a2q, const double*
     }
 }
 
-__device__ __forceinline__ void l2_prefetch(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-#ifndef SWEEP_L2PF
-#define SWEEP_L2PF 0  // measured slower (profiles/r01d/sweep_variants/README.md)
-#endif
-__device__ __forceinline__ constexpr bool sweep_l2_prefetch() { return SWEEP_L2PF != 0; }
-
 // U consecutive values of a stream (U = 2: one 128-bit load, U = 4: two)
 template <typename CT, int U>
 __device__ __forceinline__ void ldU(const CT* p, double* o) {
@@ -967,26 +959,10 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
                 t = __ldg(reinterpret_cast<const double2*>(a.hi + bk)); chi[i][0] = t.x; chi[i][1] = t.y;
             }
         } else if constexpr (U == 4) {
-            // staged: x, y, v into this thread's slab slots; coefficients read at use,
-            // after an L2 prefetch issued here (one per 128-byte line) so that the
-            // reads at use are L2 hits instead of serialised HBM round trips
+            // staged: x, y, v into this thread's slab slots; coefficients read at use
+            // (an L2 prefetch of them here measured slower, profiles/r01d)
             double* slab = reinterpret_cast<double*>(pf_sm);
             const int bsz = blockDim.x;
-            if ((tid & 3) == 0 && sweep_l2_prefetch()) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    const long long e = (long long)i * qn + j * a.n_pad + kl;
-                    if constexpr (sizeof(CT) == 4) {
-                        if ((tid & 7) == 0) {
-                            l2_prefetch(a.fa2 + e); l2_prefetch(a.fa1 + e);
-                            l2_prefetch(a.fb2 + e); l2_prefetch(a.fb1 + e);
-                        }
-                    } else {
-                        l2_prefetch(a.a2 + e); l2_prefetch(a.a1 + e);
-                        l2_prefetch(a.b2 + e); l2_prefetch(a.b1 + e);
-                    }
-                }
-            }
             double t[4];
             ldU<double, 4>(a.y + j * a.n_pad + kl, t);
             wr4(slab + ((size_t)Slab4<M>::Y * bsz + tid) * 4, t);
