@@ -1246,10 +1246,11 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     const Layout& L = ctx->L;
     KArgs& a = ctx->ka;
     {
-        // 4 cells per thread (staged through shared memory) is the default for m <= 2:
-        // 43-46 % vs 40-43 % of HBM peak at q = 1e4..1e5 (profiles/r01d); ADMM_SWEEP_CPT=2 reverts
+        // 4 cells per thread staged through shared memory (ADMM_SWEEP_CPT=4, m <= 2) is opt-in:
+        // it beat the two-cell CTA at q = 1e5 (46 vs 43 %) but the row loop below supersedes it
+        // for many rows, and at few rows the two-cell CTA is as fast (profiles/r01d, r01f)
         const char* e = getenv("ADMM_SWEEP_CPT");
-        ctx->cpt = (e && e[0] == '2') ? 2 : (m <= 2 ? 4 : 2);
+        ctx->cpt = (e && e[0] == '4' && m <= 2) ? 4 : 2;
         // row loop (128-thread CTAs own whole rows; 4 per SM): the default for m <= 2 when
         // there are rows for every CTA (q >= 4 x SMs): q = 1e4 / 1e5 at 54 / 56 % of the
         // HBM peak vs 44 / 46 % (profiles/r01e).  ADMM_SWEEP_RL = 0 off, 1 force, 6 = 64 threads

@@ -859,7 +859,9 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
     // row-level check maxima, held by thread i < M for source i
     double my_r2 = 0.0, my_r3 = 0.0, my_s1 = 0.0, my_s2 = 0.0;
 
-    if (FX) __syncthreads();  // slot counters initialised
+    // slot counters (FX) and the consensus accumulators acc[] initialised before any use
+    // (the row loop adds to acc from thread 0 before its first block barrier)
+    if (FX || RL) __syncthreads();
     long long litem = 0;
     // (row, tile) of the item, advanced incrementally (no 64-bit division per item)
     long long j = RL ? (long long)blockIdx.x : (long long)blockIdx.x / a.T;
@@ -1163,6 +1165,7 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
                 __threadfence_block();
             }
             last = __shfl_sync(0xffffffffu, last, 0);
+            __syncwarp();  // memory ordering: lane 0 acquired the slot writes, the warp reads them
             if (last) {
                 // ---- this warp arrived last: row finalisation (6b),(6g),(6d),(6i)
                 if (lane < M) {

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(StreamCfg<M>::TL, 1) sweep_tma_kernel(KArgs a,
                 __threadfence_block();
             }
             last = __shfl_sync(0xffffffffu, last, 0);
+            __syncwarp();  // memory ordering: lane 0 acquired the slot writes, the warp reads them
             if (last) {
                 if (lane < M) {
                     const int i = lane;

@@ -8,16 +8,21 @@ cases = [("toy", synth.toy_problem()), ("phev q3 n200", synth.phev_problem(200, 
          ("random m3 n37 q3", synth.random_problem(3, 37, 3, seed=5)),
          ("random m2 n1025 q2", synth.random_problem(2, 1025, 2, seed=6))]
 engines = [("stream", 1, {}), ("cluster", 2, {}), ("grid", 2, {"ADMM_PERSIST_GRID": "1"}),
-           ("stream_fx", 1, {"ADMM_SWEEP_FX": "1"}), ("stream_tma", 1, {"ADMM_STREAM_TMA": "1"})]
+           ("stream_fx", 1, {"ADMM_SWEEP_FX": "1"}), ("stream_tma", 1, {"ADMM_STREAM_TMA": "1"}),
+           ("stream_rl", 1, {"ADMM_SWEEP_RL": "1"}), ("stream_u4", 1, {"ADMM_SWEEP_CPT": "4"}),
+           ("stream_pf", 1, {"ADMM_SWEEP_PF": "1"}),
+           ("stream_rl_f32", 1, {"ADMM_SWEEP_RL": "1"})]
+KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA", "ADMM_SWEEP_RL", "ADMM_SWEEP_CPT",
+        "ADMM_SWEEP_PF")
 only = os.environ.get("ENGINES")
 for name, P in cases:
     for en, mode, env in engines:
         if only and en not in only.split(","):
             continue
-        for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA"):
+        for k in KEYS:
             os.environ.pop(k, None)
         os.environ.update(env)
-        s = L.AdmmSolver(P["m"], P["n"], P["q"], r_bar=1e-6 * max(1.0, float(np.nanmax(np.where(np.isfinite(P["c"]), P["c"], 0)))), exec_mode=mode)
+        s = L.AdmmSolver(P["m"], P["n"], P["q"], r_bar=1e-6 * max(1.0, float(np.nanmax(np.where(np.isfinite(P["c"]), P["c"], 0)))), exec_mode=mode, coeff_bits=32 if en.endswith("_f32") else 64)
         s.set_problem(P)
         s.iterate(25)
         S = s.state()
