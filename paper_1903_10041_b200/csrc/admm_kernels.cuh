@@ -307,11 +307,6 @@ __device__ __forceinline__ void quartic_coreU(const double* b, const double* c, 
         all = all && isfinite(De[u]) && !(De[u] > 0.0) && !(Q[u] == 0.0 && R[u] == 0.0);
     }
     if (all) {
-#ifdef SWEEP_CHEAP_TRIG  // timing experiment only (wrong results)
-#pragma unroll
-        for (int u = 0; u < U; ++u) out[u] = clampd(-b[u] + d[u], lo[u], hi[u]);
-        return;
-#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) out[u] = trig_pick<MODE>(b[u], c[u], d[u], Q[u], R[u], De[u], lo[u], hi[u]);
     } else {
@@ -823,7 +818,10 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
     const int ce = a.prm->check_every;
     const bool is_check = ce > 0 && ((it + 1) % ce) == 0;
 
-    __shared__ double red[16][(3 * M + 2) > 6 ? (3 * M + 2) : 6];
+    // red is double-buffered by the CTA's row parity in the row loop: with no trailing
+    // barrier a warp may reach the next row's reduction while warp 0 still reads this one
+    __shared__ double red2[2][16][(3 * M + 2) > 6 ? (3 * M + 2) : 6];
+    int rpar = 0;  // row loop: parity of the rows this CTA has reduced
     __shared__ double rowres[3 * M];
     __shared__ double k0x[M], k0nu[M];
     __shared__ double acc[XB];
@@ -1259,6 +1257,8 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
                 dgn[i] = warp_min(dgn[i]);
             }
         }
+        auto red = red2[rpar];
+        if (RL) rpar ^= 1;
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -1379,9 +1379,11 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
             acc[2 * MAXM + tid] = fmin(acc[2 * MAXM + tid], k0x[tid]);
         }
         __syncwarp();
-        // red/rowres/k0x reused by the next item.  RL: red is read by warp 0 before it
-        // reaches the next reduction's barrier, rowres stays within warp 0, and k0x is
-        // not used (thread 0 adds the consensus term itself), so no barrier is needed
+        // red/rowres/k0x reused by the next item.  RL: red alternates between two
+        // buffers by row parity (warp 0 reads red[p] of row r before it arrives at row
+        // r+1's barrier, so no warp can write red[p] again for row r+2 before that read),
+        // rowres stays within warp 0, and k0x is not used (thread 0 adds the consensus
+        // term itself), so no barrier is needed
         if (!(RL && a.T > 1)) __syncthreads();
     }
 
@@ -1395,6 +1397,7 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
         my_r3 = warp_max(my_r3);
         my_s1 = warp_max(my_s1);
         my_s2 = warp_max(my_s2);
+        auto red = red2[0];
         if (lane == 0) {
             red[wid][0] = my_r1;
             red[wid][1] = my_s3;
