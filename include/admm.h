@@ -86,7 +86,7 @@ typedef enum {
     ADMM_ENGINE_STREAM = 1,      /* sweep_kernel: one launch per iteration (graph while loop) */
     ADMM_ENGINE_GRID = 2,        /* persist_kernel: one cooperative launch per call */
     ADMM_ENGINE_CLUSTER = 3,     /* persist_cluster_kernel: one cluster launch per call */
-    ADMM_ENGINE_STREAM_TMA = 4   /* sweep_tma_kernel (opt-in: env ADMM_STREAM_TMA=1) */
+    ADMM_ENGINE_STREAM_TMA = 4   /* sweep2_kernel: TMA-fed streaming sweep, one launch per iteration (default for finite boxes) */
 } admm_engine;
 
 /* Scenario sharding across ranks (one process per GPU).  Rank r owns the
@@ -135,8 +135,13 @@ size_t admm_workspace_bytes(int32_t m, int64_t n, int64_t q_local, int32_t devic
 /* NCCL unique id for a multi-GPU context (call on rank 0 only). */
 admm_status admm_nccl_unique_id(unsigned char out[128]);
 
-/* Create a context for m sources, n steps, q_total scenarios.  dist = NULL:
-   single GPU, all scenarios local.  workspace: device buffer of at least
+/* Create a context for m sources, n steps, q_total scenarios of the robust
+   problem Eq. (2) (variables and multipliers of its ADMM form
+   Eq. (5)).  dist = NULL: single GPU, all scenarios local.
+   Errors: ADMM_ERR_INVALID for m not in 1..4, n or q_total <= 0, a bad shard;
+   ADMM_ERR_CUDA / ADMM_ERR_NCCL if the device or communicator cannot be set
+   up (*ctx is then NULL).  The caller owns the workspace; the context owns
+   everything it creates and frees it in admm_destroy.  workspace: device buffer of at least
    admm_workspace_bytes bytes (NULL: the library allocates).  cuda_stream:
    cudaStream_t to order all work on (NULL = the legacy default stream). */
 admm_status admm_create(admm_ctx** ctx, int32_t m, int64_t n, int64_t q_total,
@@ -163,17 +168,33 @@ admm_status admm_reset(admm_ctx* ctx);
 admm_status admm_set_params(admm_ctx* ctx, const admm_params* params);
 admm_status admm_get_params(const admm_ctx* ctx, admm_params* out);
 
-/* Exactly `iters` iterations; checks and rho adaptation at every multiple of
-   check_every (counted over the context's lifetime), never stops early. */
+/* Exactly `iters` ADMM iterations, each the updates (6a)-(6i) of PAPER.md:421-450
+   in printed order (readings G1-G21): the per-element quartic of
+   (6a) minimised in closed form by Algorithm 1 and boxed,
+   the capacity sums (6b)/(6d)/(6g)/(6i), the consensus (6c)/(6h), the demand
+   slack (6e)/(6f).  At every multiple of check_every (counted over the
+   context's lifetime) the residuals r and sigma are
+   evaluated and rho adapted by the 1.2 / 0.8 band rule (PAPER.md:318-324,
+   checked every 10 iterations :353); never stops early.  Asynchronous with
+   respect to the host only up to one device->host read of the iteration
+   counter at the end of the call.  ADMM_ERR_STATE before admm_set_problem,
+   ADMM_ERR_NUMERICAL if a check saw NaN/Inf (the state then stops changing). */
 admm_status admm_iterate(admm_ctx* ctx, int64_t iters);
 
-/* Iterate until a check finds r < r_bar and sigma < sigma_bar (ADMM_OK) or
-   max_iter more iterations are done (ADMM_NOT_CONVERGED).  info may be NULL. */
+/* Iterate as admm_iterate until a check finds r < r_bar and sigma < sigma_bar
+   (the termination rule of PAPER.md:353, :464-479; thresholds r_bar = 1e-6 dE,
+   sigma_bar = 1e-2 in the paper's experiments) -> ADMM_OK, or
+   max_iter more iterations are done -> ADMM_NOT_CONVERGED.  The whole loop
+   runs on the device (CUDA-graph WHILE node; no host round trip per
+   iteration).  info may be NULL. */
 admm_status admm_solve(admm_ctx* ctx, double r_bar, double sigma_bar, int64_t max_iter,
                        admm_info* info);
 
-/* Solution: x [m][q_local][n] and x1 [m] (either may be NULL), info (may be NULL,
-   objective included). */
+/* Solution of the ADMM iterate: x = x_k^{(i,j)} [m][q_local][n] (row-major,
+   k fastest) and the consensus first move x1^{(i)} [m] of (6c) (PAPER.md:436,
+   mean reading G1), either may be NULL; info (may be NULL) with the objective
+   (1/q) sum_{i,j,k} f(x) of Eq. (2) (reading G20).  Outputs are
+   caller-allocated; on_device = 1 for device pointers.  Synchronous. */
 admm_status admm_get_solution(admm_ctx* ctx, double* x, double* x1, admm_info* info,
                               int32_t on_device);
 
@@ -223,10 +244,15 @@ admm_status admm_get_coeff_precision(const admm_ctx* ctx, int32_t* bits);
 const char* admm_last_error(const admm_ctx* ctx);
 void admm_destroy(admm_ctx* ctx);
 
-/* Algorithm 1 on a batch (microbench, BASELINE.json configs[4]):
-   x[e] = boxmin of A x^4 + B x^3 + C x^2 + D x over [lo[e], hi[e]] (box_mode),
-   A >= 0.  All arrays are DEVICE pointers of length N; lo/hi may be NULL
-   (unbounded).  Asynchronous on cuda_stream. */
+/* Algorithm 1 of PAPER.md:170-198 (closed-form minimiser of a quartic through the
+   roots of its derivative cubic: Cardano / trigonometric / Vieta branches,
+   PAPER.md:129-165, with the stable forms G4-G9 of DESIGN.md §3) on a batch:
+   x[e] = the minimiser of A x^4 + B x^3 + C x^2 + D x, then the box step of
+   (6a) (box_mode PROJECT = clamp of the global minimiser,
+   EXACT = minimiser over [lo[e], hi[e]], reading G3).  A >= 0 (A = 0: the
+   convex quadratic).  All arrays are DEVICE pointers of length N (caller
+   owned); lo/hi may be NULL (unbounded).  Asynchronous on cuda_stream;
+   ADMM_ERR_INVALID for N < 0, NULL A..D / x or a bad box_mode. */
 admm_status quartic_minimize_batch(const double* A, const double* B, const double* C,
                                    const double* D, const double* lo, const double* hi,
                                    double* x, int64_t N, int32_t box_mode, void* cuda_stream);

@@ -16,6 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
+_SO_OMP = os.path.join(_HERE, "liboracle_omp.so")  # same source, OpenMP loops (CPU-parallel baseline)
 _SRC = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "oracle.h")]
 
 BOX_PROJECT, BOX_EXACT = 0, 1
@@ -27,19 +28,21 @@ PAPER_TAU = 1.1
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (plain C, -O2 -ffp-contract=off)."""
-    if not force and os.path.exists(_SO):
-        so_m = os.path.getmtime(_SO)
-        if all(os.path.getmtime(s) <= so_m for s in _SRC):
-            return _SO
-    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC",
-           "-shared", "-o", _SO + ".tmp", _SRC[0], "-lm"]
-    subprocess.check_call(cmd)
-    os.replace(_SO + ".tmp", _SO)
+    """Compile liboracle.so (serial) and liboracle_omp.so (the same source with its
+    OpenMP loops on) with gcc (plain C, -O2 -ffp-contract=off)."""
+    for so, extra in ((_SO, []), (_SO_OMP, ["-fopenmp"])):
+        if not force and os.path.exists(so):
+            so_m = os.path.getmtime(so)
+            if all(os.path.getmtime(s) <= so_m for s in _SRC):
+                continue
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC",
+               *extra, "-shared", "-o", so + ".tmp", _SRC[0], "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(so + ".tmp", so)
     return _SO
 
 
-_lib = None
+_libs = {}
 
 
 class _Problem(C.Structure):
@@ -71,11 +74,15 @@ class _Info(C.Structure):
 REDUCE_FN = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_int, C.c_int, C.c_void_p)
 
 
-def lib():
-    global _lib
+def lib(omp: bool = False):
+    """The serial oracle, or (omp=True) its OpenMP build; bitwise-identical results."""
+    _lib = _libs.get(omp)
     if _lib is None:
-        _lib = C.CDLL(build())
+        build()
+        _lib = _libs[omp] = C.CDLL(_SO_OMP if omp else _SO)
         d = C.c_double
+        _lib.orc_set_threads.argtypes = [C.c_int]
+        _lib.orc_set_threads.restype = C.c_int
         pd = C.POINTER(C.c_double)
         _lib.orc_cubic_roots.argtypes = [d, d, d, pd, C.POINTER(C.c_int)]
         _lib.orc_cubic_roots.restype = C.c_int
@@ -126,7 +133,12 @@ def quartic_boxmin(A, B, Cc, D, lo, hi, mode=BOX_PROJECT):
     return x, bool(t.value)
 
 
-def quartic_batch(A, B, Cc, D, lo=None, hi=None, mode=BOX_PROJECT):
+def set_threads(n: int) -> int:
+    """Threads of the OpenMP build (bench.py's CPU-parallel baseline); returns the count."""
+    return lib(omp=True).orc_set_threads(int(n))
+
+
+def quartic_batch(A, B, Cc, D, lo=None, hi=None, mode=BOX_PROJECT, omp=False):
     A, B, Cc, D = map(_f64, (A, B, Cc, D))
     N = A.size
     x = np.empty(N)
@@ -134,8 +146,8 @@ def quartic_batch(A, B, Cc, D, lo=None, hi=None, mode=BOX_PROJECT):
     keep = (_f64(lo) if lo is not None else None, _f64(hi) if hi is not None else None)
     lo_p = _p(keep[0]) if lo is not None else None
     hi_p = _p(keep[1]) if hi is not None else None
-    lib().orc_quartic_batch(_p(A), _p(B), _p(Cc), _p(D), lo_p, hi_p, _p(x), N, mode,
-                            C.byref(ties))
+    lib(omp).orc_quartic_batch(_p(A), _p(B), _p(Cc), _p(D), lo_p, hi_p, _p(x), N, mode,
+                               C.byref(ties))
     return x, ties.value
 
 
@@ -161,9 +173,11 @@ class Oracle:
 
     prob: dict from synth (m, n, q, a2.., lo, hi, y, c).  q_total defaults to
     prob['q'].  reduce: optional python callable reduce(np_array, op) that
-    all-reduces in place (op 0 = sum, 1 = max) -- used by the gloo tests."""
+    all-reduces in place (op 0 = sum, 1 = max) -- used by the gloo tests.
+    omp: run on the OpenMP build (bitwise-identical results, CPU-parallel baseline)."""
 
-    def __init__(self, prob, params=None, q_total=None, reduce=None):
+    def __init__(self, prob, params=None, q_total=None, reduce=None, omp=False):
+        self._lib = lib(omp)
         self.prob = {k: (_f64(v) if isinstance(v, np.ndarray) else v) for k, v in prob.items()}
         P = self.prob
         m, n, q = int(P["m"]), int(P["n"]), int(P["q"])
@@ -189,9 +203,9 @@ class Oracle:
         else:
             self._cb = REDUCE_FN()
         msg = C.create_string_buffer(256)
-        if lib().orc_validate(C.byref(self._P), msg, 256) != 0:
+        if self._lib.orc_validate(C.byref(self._P), msg, 256) != 0:
             raise ValueError(msg.value.decode())
-        lib().orc_init(C.byref(self._P), C.byref(self._S), C.byref(self._prm), self._cb, None)
+        self._lib.orc_init(C.byref(self._P), C.byref(self._S), C.byref(self._prm), self._cb, None)
 
     def _mk_params(self):
         p = self.params
@@ -212,7 +226,7 @@ class Oracle:
             hist_cap = iters // max(1, self.params["check_every"]) + 1
         hist = np.zeros((max(1, hist_cap), HIST_COLS))
         info = _Info()
-        lib().orc_run(C.byref(self._P), C.byref(self._S), C.byref(self._prm), int(iters),
+        self._lib.orc_run(C.byref(self._P), C.byref(self._S), C.byref(self._prm), int(iters),
                       int(bool(stop_on_converge)), C.byref(info), _p(hist), hist_cap, self._cb,
                       None)
         rows = min(info.hist_rows, hist_cap)
@@ -225,7 +239,7 @@ class Oracle:
 
     def objective(self, x=None):
         x = self.x if x is None else _f64(x)
-        return lib().orc_objective(C.byref(self._P), _p(x), self._cb, None)
+        return self._lib.orc_objective(C.byref(self._P), _p(x), self._cb, None)
 
     def state(self):
         return {k: getattr(self, k).copy() for k in

@@ -10,8 +10,27 @@
 
 #include <math.h>
 #include <stdio.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
+
+/* OpenMP build (liboracle_omp.so, the "CPU-parallel" baseline of bench.py):
+   the loops over independent (j,k) cells and (i,j) rows are shared out over
+   threads; every sum stays serial inside its row and every max is
+   order-independent, so the results are bitwise those of the serial build.
+   orc_set_threads is a no-op in the serial build. */
+int orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
 
 /* ------------------------------------------------------------------------- */
 /* small helpers                                                             */
@@ -216,6 +235,7 @@ void orc_quartic_batch(const double *A, const double *B, const double *C, const 
                        long *ties)
 {
     long t = 0;
+#pragma omp parallel for reduction(+ : t) schedule(static)
     for (long e = 0; e < N; ++e) {
         int tie = 0;
         x[e] = orc_quartic_boxmin(A[e], B[e], C[e], D[e], lo ? lo[e] : -INFINITY,
@@ -403,6 +423,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
            the latest values of the other sources (Gauss-Seidel, reading G2).
            theta uses lambda^{(i,j)}_k (erratum E5). */
         for (int i = 0; i < m; ++i)
+#pragma omp parallel for reduction(+ : ties) schedule(static)
             for (long j = 0; j < q; ++j)
                 for (long k = 0; k < n; ++k) {
                     long e = IX(i, j, k);
@@ -423,6 +444,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
         /* (6b) PAPER.md:431-434: z = w + rho2/(rho1 + n rho2) 1 (h + p - 1'w),
            w = g(x) - lambda */
         double kap = rho[1] / (rho[0] + (double)n * rho[1]);
+#pragma omp parallel for collapse(2) schedule(static)
         for (int i = 0; i < m; ++i)
             for (long j = 0; j < q; ++j) {
                 nsum a = {0, 0};
@@ -450,6 +472,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
         for (int i = 0; i < m; ++i) S->x1[i] = buf[i] / qd;
 
         /* (6d) PAPER.md:438: h = min(c, 1'z - p) */
+#pragma omp parallel for collapse(2) schedule(static)
         for (int i = 0; i < m; ++i)
             for (long j = 0; j < q; ++j) {
                 nsum a = {0, 0};
@@ -460,6 +483,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
 
         /* (6e) PAPER.md:440: s = max(0, sum_i x - y - mu);
            (6f) PAPER.md:442: mu = mu + s - sum_i x + y */
+#pragma omp parallel for schedule(static)
         for (long j = 0; j < q; ++j)
             for (long k = 0; k < n; ++k) {
                 double sx = 0.0;
@@ -467,6 +491,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                 long c = JK(j, k);
                 S->s[c] = fmax(0.0, sx - P->y[c] - S->mu[c]);
             }
+#pragma omp parallel for schedule(static)
         for (long j = 0; j < q; ++j)
             for (long k = 0; k < n; ++k) {
                 double sx = 0.0;
@@ -475,6 +500,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                 S->mu[c] = S->mu[c] + S->s[c] - sx + P->y[c];
             }
         /* (6g) PAPER.md:444: lambda = lambda + z - g(x) */
+#pragma omp parallel for schedule(static)
         for (size_t e = 0; e < NE; ++e) S->lam[e] = S->lam[e] + S->z[e] - gfun(P, (long)e, S->x[e]);
         /* (6h) PAPER.md:446: nu = nu + x1 - x_1^{(i,j)} */
         for (int i = 0; i < m; ++i)
@@ -491,7 +517,9 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
         /* residual check every check_every iterations */
         if (prm->check_every > 0 && S->iter % prm->check_every == 0) {
             double t[7] = {0, 0, 0, 0, 0, 0, 0};
+            double t0 = 0.0, t1 = 0.0, t4 = 0.0, t6 = 0.0;
             /* r, erratum E6 / reading G14: max over all indices */
+#pragma omp parallel for reduction(max : t0, t6) schedule(static)
             for (long j = 0; j < q; ++j)
                 for (long k = 0; k < n; ++k) {
                     double sx = 0.0, dx = 0.0;
@@ -500,14 +528,19 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                         dx += S->x[IX(i, j, k)] - xt[IX(i, j, k)];
                     }
                     long c = JK(j, k);
-                    t[0] = fmax(t[0], fabs(S->s[c] - sx + P->y[c]));
+                    t0 = fmax(t0, fabs(S->s[c] - sx + P->y[c]));
                     /* sigma 3rd term: ||(s - s~) - sum_i (x - x~)|| */
-                    t[6] = fmax(t[6], fabs((S->s[c] - st[c]) - dx));
+                    t6 = fmax(t6, fabs((S->s[c] - st[c]) - dx));
                 }
+#pragma omp parallel for reduction(max : t1, t4) schedule(static)
             for (size_t e = 0; e < NE; ++e) {
-                t[1] = fmax(t[1], fabs(S->z[e] - gfun(P, (long)e, S->x[e])));
-                t[4] = fmax(t[4], fabs(S->z[e] - zt[e]));
+                t1 = fmax(t1, fabs(S->z[e] - gfun(P, (long)e, S->x[e])));
+                t4 = fmax(t4, fabs(S->z[e] - zt[e]));
             }
+            t[0] = t0;
+            t[1] = t1;
+            t[4] = t4;
+            t[6] = t6;
             for (int i = 0; i < m; ++i)
                 for (long j = 0; j < q; ++j) {
                     t[2] = fmax(t[2], fabs(S->h[IJ(i, j)] - sz[IJ(i, j)]));

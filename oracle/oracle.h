@@ -88,6 +88,9 @@ void orc_build_quartic(double a2, double a1, double b2, double b1, double b0, do
 
 /* ADMM */
 int orc_validate(const orc_problem *P, char *msg, int msglen);
+/* OpenMP build only: threads for the parallel loops (returns the count in use;
+   the serial build returns 1) */
+int orc_set_threads(int n);
 void orc_init(const orc_problem *P, orc_state *S, const orc_params *prm,
               orc_reduce_fn reduce, void *user);
 int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iters,

@@ -226,7 +226,7 @@ def admm_get_timing(ctx):
 
 
 ENGINE_NAMES = {0: "none", 1: "sweep_kernel", 2: "persist_kernel", 3: "persist_cluster_kernel",
-                4: "sweep_tma_kernel"}
+                4: "sweep2_kernel"}
 
 
 def admm_get_engine(ctx):

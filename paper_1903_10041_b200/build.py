@@ -35,26 +35,45 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
-    """out/defines: experimental variants (e.g. -DSWEEP_LB=1024) written next to the
-    product library and loaded with ADMM_SO=<path>; the product build takes neither."""
+    """Compile every csrc/*.cu translation unit (in parallel) and link the shared
+    library.  out/defines: experimental variants (e.g. -DSWEEP2_MINB=3) written next
+    to the product library and loaded with ADMM_SO=<path>; the product build takes
+    neither."""
     SO = out or globals()["SO"]
     if not out and not force and up_to_date():
         return SO
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
-           *[f"-D{d}" for d in defines],
-           "-o", SO + ".tmp", os.path.join(CSRC, "admm.cu")]
+    odir = os.path.join(HERE, "build", "obj" if not out else "obj_" + os.path.basename(out))
+    os.makedirs(odir, exist_ok=True)
+    common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
+              *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    r = subprocess.run(cmd, capture_output=True, text=True)
+        common.insert(1, "-Xptxas=-v")
+    units = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    procs, objs = [], []
+    for u in units:
+        o = os.path.join(odir, os.path.basename(u)[:-3] + ".o")
+        objs.append(o)
+        procs.append((u, subprocess.Popen(common + ["-c", "-o", o, u], stdout=subprocess.PIPE,
+                                          stderr=subprocess.PIPE, text=True)))
+    failed = False
+    for u, p in procs:
+        so, se = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(f"--- {u}\n" + so + se)
+            failed = True
+        elif verbose:
+            sys.stderr.write(se)
+    if failed:
+        raise RuntimeError("nvcc failed building libadmm_b200.so")
+    link = [nvcc, *ARCH, "-shared", "-o", SO + ".tmp", *objs,
+            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}"]
+    r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libadmm_b200.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libadmm_b200.so")
     os.replace(SO + ".tmp", SO)
     return SO
 

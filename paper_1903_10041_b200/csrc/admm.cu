@@ -26,7 +26,7 @@
 #include "admm_kernels.cuh"
 #include "admm_persist.cuh"
 #include "admm_onchip.cuh"
-#include "admm_stream.cuh"
+#include "admm_sweep2.cuh"
 
 using namespace admm_dev;
 
@@ -485,12 +485,14 @@ struct admm_ctx {
     bool prep_ok = false;         // bq / ib2s valid (on-chip-sized problems)
     bool fx_ok = false;           // fixed-point scales of the row sums valid (finite bounds)
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
-    bool use_tma = false;         // streaming engine: TMA-pipelined sweep (else legacy sweep)
+    bool use_tma = false;         // streaming engine: the TMA sweep (sweep2_kernel) runs
+    const void* s2_fn = nullptr;  // sweep2_kernel instantiation of the current plan
+    size_t s2_smem = 0;           // its dynamic shared memory (the stage ring)
     int coeff_bits = 64;          // F2: storage precision of a2, a1, b2, b1 (64 or 32)
     int cpt = 2;                  // streaming sweep: cells per thread (2, or 4 for m <= 2)
     int rl = 0;                   // streaming sweep: row loop, CTA size (0 = off, 128 or 64)
     bool graph_dirty = true;      // problem changed since the graph was captured
-    SArgs sa{};
+    S2Args s2{};
 };
 
 namespace {
@@ -550,7 +552,6 @@ __global__ void round_coeff_kernel(long long NE, double* a2, double* a1, double*
 }
 
 typedef void (*sweep_fn)(KArgs);
-typedef void (*sweep_tma_fn)(KArgs, SArgs);
 
 // Barrier-free (fixed-point, last-warp-finalises) sweep for rows spanning several
 // tiles (horizon n = 1e6: 26 -> 34 % of HBM peak); the barrier variant stays for
@@ -633,75 +634,47 @@ sweep_fn pick_sweep(int m, int mode, bool fx, bool f32, bool pf, int cpt, int rl
 bool use_pf_sweep(const admm_ctx* ctx);
 size_t pf_smem_bytes(const admm_ctx* ctx);
 
-sweep_tma_fn pick_sweep_tma(int m, int mode, int* tl, size_t* smem) {
-#define S(MM)                                                                                  \
-    if (m == MM) {                                                                             \
-        *tl = StreamCfg<MM>::TL;                                                               \
-        *smem = StreamCfg<MM>::SMEM;                                                           \
-        return mode == BOX_EXACT ? sweep_tma_kernel<MM, BOX_EXACT> : sweep_tma_kernel<MM, BOX_PROJECT>; \
-    }
-    S(1) S(2) S(3) S(4)
-#undef S
-    return nullptr;
-}
-
-// streaming engine configuration: TMA sweep when the fixed-point scales exist
+// streaming engine: the TMA sweep (admm_sweep2.cuh) whenever the fixed-point row
+// scales exist (finite boxes) and m <= 4; ADMM_SWEEP2=0 selects the register-fed
+// sweep_kernel (kept for infinite bounds and as a measured alternative)
 admm_status plan_stream(admm_ctx* ctx) {
-    int tl = 0;
+    ctx->use_tma = false;
+    const char* opt = getenv("ADMM_SWEEP2");
+    if (opt && opt[0] == '0') return ADMM_OK;
+    if (!ctx->fx_ok || ctx->m > 4) return ADMM_OK;
+    int ns = 0;
     size_t smem = 0;
-    sweep_tma_fn tf = pick_sweep_tma(ctx->m, ctx->params.box_mode, &tl, &smem);
-    // The TMA-pipelined sweep (admm_stream.cuh) is opt-in: on B200 the register-
-    // bound 2-cells-per-thread sweep_kernel measured faster (44-47 % vs 37 % of
-    // HBM peak at q = 1e4..1e5, profiles/README.md), the fp64 chain latency and
-    // not the load/compute overlap being the limiter.
-    const char* opt = getenv("ADMM_STREAM_TMA");
-    ctx->use_tma = tf && ctx->fx_ok && (opt && opt[0] == '1') && ctx->coeff_bits == 64;
-    if (!ctx->use_tma) return ADMM_OK;
-    if (cudaFuncSetAttribute((const void*)tf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-        cudaGetLastError();
-        ctx->use_tma = false;
-        return ADMM_OK;
-    }
+    const void* fn = sweep2_pick(ctx->m, ctx->params.box_mode, ctx->coeff_bits / 8, &ns, &smem);
+    if (!fn) return ADMM_OK;
+    CKC(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, S2_NT, smem));
+    if (occ < 1) return ADMM_OK;
+    occ = std::min(occ, 32);
+    ctx->s2 = sweep2_plan(ctx->q, ctx->n_pad, occ * ctx->sms);
+    ctx->s2_fn = fn;
+    ctx->s2_smem = smem;
+    ctx->use_tma = true;
     if (const char* dbg = getenv("ADMM_DEBUG")) {
         if (dbg[0] == '1') {
             cudaFuncAttributes fa;
-            if (cudaFuncGetAttributes(&fa, (const void*)tf) == cudaSuccess)
-                fprintf(stderr, "[admm] sweep_tma: regs %d maxThreads %d static smem %zu dyn max %d local %zu\n",
-                        fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
-                        fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+            if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess)
+                fprintf(stderr, "[admm] sweep2: regs %d local %zu smem %zu+%zu occ %d G %d S %d TPS %d TPR %d\n",
+                        fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes, smem, occ, ctx->s2.G, ctx->s2.S,
+                        ctx->s2.TPS, ctx->s2.TPR);
         }
     }
-    SArgs& sa = ctx->sa;
-    sa.TL = tl;
-    sa.TPR = (int)((ctx->n + tl - 1) / tl);
-    sa.G = ctx->sms;
-    // rows are split into S segments only when there are too few rows to balance the SMs
-    const long long q = ctx->q;
-    sa.S = q >= 8LL * sa.G ? 1 : (int)std::min<long long>(sa.TPR, (8LL * sa.G + q - 1) / q);
-    sa.TPS = (sa.TPR + sa.S - 1) / sa.S;
-    sa.S = (sa.TPR + sa.TPS - 1) / sa.TPS;
-    sa.U = (int)(q * sa.S);
-    for (int i = 0; i < MAXM; ++i) {
-        sa.fx_scale[i] = ctx->fx_scale[i];
-        sa.fx_inv[i] = ctx->fx_inv[i];
-    }
-    sa.rowacc = (unsigned long long*)(ctx->ws + ctx->L.rowacc);
-    sa.rowdg = (unsigned long long*)(ctx->ws + ctx->L.rowdg);
-    sa.rowcnt = (unsigned*)(ctx->ws + ctx->L.rowcnt);
     return ADMM_OK;
 }
 
 // body of one while-loop pass: check_every iterations
 admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
     const int K = std::max(1, ctx->params.check_every);
-    int tl = 0;
-    size_t smem = 0;
-    sweep_tma_fn tf = pick_sweep_tma(ctx->m, ctx->params.box_mode, &tl, &smem);
     for (int r = 0; r < K; ++r) {
-        if (ctx->use_tma)
-            tf<<<ctx->sa.G, ctx->sa.TL, smem, st>>>(ctx->ka, ctx->sa);
-        else
+        if (ctx->use_tma) {
+            void* args[] = {(void*)&ctx->ka, (void*)&ctx->s2};
+            CKC(cudaLaunchKernel(ctx->s2_fn, dim3((unsigned)ctx->s2.G), dim3(S2_NT), args, ctx->s2_smem, st));
+        } else
             fn<<<ctx->G, ctx->bs, pf_smem_bytes(ctx), st>>>(ctx->ka);
         CKC(cudaGetLastError());
         if (ctx->world > 1) {
@@ -1382,6 +1355,7 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
         CKC(cudaMemcpyAsync(keys, gb, MAXM * 8, cudaMemcpyDeviceToHost, ctx->stream));
         CKC(cudaStreamSynchronize(ctx->stream));
         bool ok = true;
+        ctx->ka.gfree = 0u;
         for (int i = 0; i < ctx->m; ++i) {
             const unsigned long long k = keys[i];
             unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
@@ -1394,6 +1368,7 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             }
             int E = 0;
             if (G > 0.0) E = 62 - (int)std::ceil(std::log2(G));
+            else ctx->ka.gfree |= 1u << i;
             E = std::max(-1000, std::min(1000, E));
             ctx->fx_scale[i] = std::ldexp(1.0, E);
             ctx->fx_inv[i] = std::ldexp(1.0, -E);

@@ -84,6 +84,7 @@ struct KArgs {
     unsigned long long *rowacc;  // [q][MAXM]
     unsigned long long *rowdg;   // [q][2 MAXM] ordered keys (checks)
     unsigned *rowcnt;            // [q][MAXM]
+    unsigned gfree;              // bit i: g^{(i)} = 0 on the box (row sums 0, no capacity bookkeeping)
     // F2: fp32 copies of the per-element coefficients, read by the
     // streaming sweep when the context stores coefficients in fp32 (admm_set_coeff_precision)
     const float *fa2, *fa1, *fb2, *fb1;          // [m][q][n_pad]
@@ -602,7 +603,7 @@ __device__ __forceinline__ void write_hist(double* h, long long it1, double r, d
 // Consumes the per-rank aggregates (rank order), computes (6c), the residuals
 // r / sigma, the termination test and the rho adaptation, and writes the next
 // control block.  Runs on one thread.
-__device__ void finalize_global(const KArgs& a, const double* agg, int world, long long it,
+__device__ inline void finalize_global(const KArgs& a, const double* agg, int world, long long it,
                                 const Ctrl& cin, Ctrl& cout, bool is_check) {
     const DParams& P = *a.prm;
     const int m = a.m;
@@ -1485,6 +1486,7 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
     }
 }
 
+#ifndef ADMM_KERNELS_NO_GLOBALS  // translation units other than admm.cu (sweep2.cu)
 // multi-GPU: after ncclAllGather(xsend -> xall) on the stream
 __global__ void finalize_kernel(KArgs a) {
     const long long it = *(volatile long long*)a.iter;
@@ -1497,5 +1499,6 @@ __global__ void finalize_kernel(KArgs a) {
     __threadfence();
     *(volatile long long*)a.iter = it + 1;
 }
+#endif
 
 }  // namespace admm_dev

@@ -1,0 +1,594 @@
+// admm_sweep2.cuh -- the streaming ADMM sweep for problems that live in HBM
+// (BASELINE.json configs[3] q >= 1e3, configs[2] n >= 1e5): one launch = one
+// ADMM iteration, Appendix A Eq. (6a)-(6i) with the residuals of
+// :464-479 on check iterations.  DESIGN.md §6 "TMA streaming sweep".
+//
+// Structure (B200):
+//  * persistent grid of 128-thread CTAs, several per SM (4 at m = 2), each
+//    owning whole work units (a scenario row j, or a segment of a long row)
+//    in a fixed order: deterministic;
+//  * every warp streams its own chunks of 64 cells (chunk c of a unit belongs
+//    to warp c mod 4) HBM -> shared memory with 1-D TMA bulk copies
+//    (cp.async.bulk + mbarrier complete_tx) into a private NS-stage ring issued
+//    by its lane 0: the fp64 work of chunk c overlaps the HBM reads of the
+//    warp's next chunks without holding registers for loads in flight, and no
+//    warp ever waits for another one (no barrier, no shared ring);
+//  * two cells per thread: Gauss-Seidel over the sources (6a) with Algorithm 1
+//    on both cells interleaved, (6e)/(6f) in the thread (identity I2),
+//    x and v written back with 128-bit stores;
+//  * the row sum sum_k (b2 x^2 + b1 x) of (6b) is accumulated per thread in
+//    exact 64-bit fixed point across the unit's tiles, warp-summed with
+//    redux.sync limbs, and the last warp to reach the unit's end finalises
+//    the row ((6b), (6g), (6d), (6i) via identity I1) -- no block barrier in
+//    the sweep; rows split into segments add their sums with integer atomics
+//    and the last segment finalises (order-independent => deterministic);
+//  * (6c) consensus partials (thread 0 owns k = 0 of every row it streams)
+//    and the residual maxima are reduced by the last CTA in CTA order, which
+//    also runs the check / rho adaptation and writes the next control block.
+#pragma once
+#include "admm_kernels.cuh"
+
+namespace admm_dev {
+
+struct S2Args {
+    int TPR;      // chunks per row (ceil(n_pad / 64))
+    int S;        // segments per row
+    int TPS;      // chunks per segment
+    int G;        // grid size
+    long long U;  // work units = q * S
+};
+
+constexpr int S2_NT = 128;  // threads per CTA
+constexpr int S2_NW = S2_NT / 32;
+constexpr int S2_TL = 64;   // cells per chunk (two per lane of one warp)
+constexpr int S2_UB = 4;    // unit slots of the row partials (flow-controlled by s_gen)
+
+// one stage of a warp's ring: x_i (M, fp64), y, v (fp64), then a2_i, a1_i, b2_i, b1_i (CT)
+template <int M, typename CT>
+struct S2Cfg {
+    static constexpr int YOFF = M * S2_TL * 8;
+    static constexpr int VOFF = (M + 1) * S2_TL * 8;
+    static constexpr int COFF = (M + 2) * S2_TL * 8;
+    static constexpr int STAGE = COFF + 4 * M * S2_TL * (int)sizeof(CT);
+};
+
+__device__ __forceinline__ unsigned s2_smem(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void s2_bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void s2_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s2_smem(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool s2_try(unsigned long long* bar, unsigned phase) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(s2_smem(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void s2_wait(unsigned long long* bar, unsigned phase) {
+    while (!s2_try(bar, phase)) {
+    }
+}
+__device__ __forceinline__ void s2_tma(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            s2_smem(dst)),
+        "l"(src), "r"(bytes), "r"(s2_smem(bar))
+        : "memory");
+}
+
+// position in one warp's chunk sequence: units u = blockIdx.x, + G, ...; chunks
+// cs + wid, + NW, ... < ce of unit u (row j); units without a chunk for this warp
+// are skipped
+struct S2Pos {
+    long long u, j;
+    int c, ce;
+    __device__ __forceinline__ void set(const S2Args& s, int wid) {
+        while (u < s.U) {
+            int cs;
+            if (s.S == 1) {
+                j = u;
+                cs = 0;
+                ce = s.TPR;
+            } else {
+                j = u / s.S;
+                cs = (int)(u - j * s.S) * s.TPS;
+                ce = min(s.TPR, cs + s.TPS);
+            }
+            c = cs + wid;
+            if (c < ce) return;
+            u += s.G;
+        }
+    }
+    __device__ __forceinline__ void next(const S2Args& s, int wid) {
+        c += S2_NW;
+        if (c >= ce) {
+            u += s.G;
+            set(s, wid);
+        }
+    }
+};
+
+template <int M, typename CT>
+__device__ __forceinline__ void s2_issue(const KArgs& a, long long j, int t, unsigned char* st,
+                                         unsigned long long* bar) {
+    using C = S2Cfg<M, CT>;
+    const int k0 = t * S2_TL;
+    const int nc = min(S2_TL, a.n_pad - k0);  // n_pad % 4 == 0: byte counts are multiples of 16
+    const unsigned b8 = (unsigned)nc * 8u, bc = (unsigned)nc * (unsigned)sizeof(CT);
+    s2_expect(bar, (unsigned)(M + 2) * b8 + 4u * M * bc);
+    const long long qn = a.q * (long long)a.n_pad;
+    const long long row = j * a.n_pad + k0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) s2_tma(st + (size_t)i * S2_TL * 8, a.x + i * qn + row, b8, bar);
+    s2_tma(st + C::YOFF, a.y + row, b8, bar);
+    s2_tma(st + C::VOFF, a.v + row, b8, bar);
+    const CT* src[4];
+    if constexpr (sizeof(CT) == 4) {
+        src[0] = a.fa2; src[1] = a.fa1; src[2] = a.fb2; src[3] = a.fb1;
+    } else {
+        src[0] = reinterpret_cast<const CT*>(a.a2); src[1] = reinterpret_cast<const CT*>(a.a1);
+        src[2] = reinterpret_cast<const CT*>(a.b2); src[3] = reinterpret_cast<const CT*>(a.b1);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            s2_tma(st + C::COFF + (size_t)(4 * i + c) * S2_TL * sizeof(CT), src[c] + i * qn + row, bc, bar);
+}
+
+// two consecutive values of a shared-memory stream (fp64 or fp32), widened
+template <typename CT>
+__device__ __forceinline__ void s2_ld2(const unsigned char* p, double* o) {
+    if constexpr (sizeof(CT) == 8) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        o[0] = t.x;
+        o[1] = t.y;
+    } else {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        o[0] = (double)t.x;
+        o[1] = (double)t.y;
+    }
+}
+
+#ifndef SWEEP2_MINB
+#define SWEEP2_MINB 4
+#endif
+
+template <int M, int MODE, typename CT, int NS>
+__global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel(KArgs a, S2Args s) {
+    using C = S2Cfg<M, CT>;
+    extern __shared__ __align__(128) unsigned char s2_sm[];
+    __shared__ __align__(8) unsigned long long s_full[S2_NW][NS];  // per-warp rings
+    __shared__ unsigned long long s_fxw[S2_UB][S2_NW][M];  // per-warp fixed-point row partials
+    __shared__ double s_dgw[S2_UB][S2_NW][2 * M];         // per-warp dg extrema (checks)
+    __shared__ unsigned s_arr[S2_UB];                      // warps arrived at the unit's end
+    __shared__ unsigned s_gen[S2_UB];                      // finalisations done per slot
+    __shared__ double s_red[S2_NW][6];
+    __shared__ double s_rc[S2_NW][M][4];   // row check terms of the finalising lanes
+    // row scalars (raw lam, zeta, p, h, sum b0, nu) of source i, per warp and unit parity:
+    // copied with cp.async by lanes i < M one unit ahead (no registers held in flight)
+    __shared__ double s_sc[S2_NW][2][6][M];
+    __shared__ double s_nue[M];            // nu after (6h), cell k = 0 (thread 0)
+    __shared__ double acc[XB];
+    __shared__ int s_last;
+
+    const long long it = *(volatile long long*)a.iter;
+    const Ctrl& cin = a.ctrl[it & 1];
+    if (cin.done || it >= a.prm->iter_limit) return;
+    const int ce = a.prm->check_every;
+    const bool chk = ce > 0 && ((it + 1) % ce) == 0;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    if (tid < XB) {
+        double init = 0.0;
+        if (tid >= MAXM && tid < MAXM + M) init = -INFINITY;        // x0max
+        if (tid >= 2 * MAXM && tid < 2 * MAXM + M) init = INFINITY;  // x0min
+        acc[tid] = init;
+    }
+    if (tid < S2_UB) {
+        s_arr[tid] = 0u;
+        s_gen[tid] = 0u;
+    }
+    if (tid < S2_NW * M * 4) (&s_rc[0][0][0])[tid] = 0.0;
+    if (tid < S2_NW * NS) {
+        s2_bar_init(&s_full[0][0] + tid);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    unsigned char* const ring = s2_sm + (size_t)wid * NS * C::STAGE;  // this warp's stages
+    S2Pos ahead;  // this warp's chunk NS positions ahead of the consumer: the refill of its stage
+    ahead.u = blockIdx.x;
+    ahead.set(s, wid);
+    for (int st = 0; st < NS && ahead.u < s.U; ++st) {
+        if (lane == 0) s2_issue<M, CT>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+        ahead.next(s, wid);
+    }
+
+    const double R1 = cin.rho[0], R3 = cin.rho[2], R4 = cin.rho[3], f2 = cin.f[2];
+    const double iq = a.inv_q;
+    const long long qn = a.q * (long long)a.n_pad;
+    const bool nu_pending = cin.nu_pending != 0;
+
+    double my_r1 = 0.0, my_s3 = 0.0;  // cell terms of the check (every thread)
+
+    int st = 0;
+    unsigned ph = 0;
+    auto fetch = [&](long long uu, int slot) {
+        if (lane < M && uu < s.U) {
+            const long long rix = (long long)lane * a.q + (s.S == 1 ? uu : uu / s.S);
+            double* d = &s_sc[wid][slot][0][lane];
+            cp_async8(d, a.lam + rix);
+            cp_async8(d + M, a.zeta + rix);
+            cp_async8(d + 2 * M, a.p + rix);
+            cp_async8(d + 3 * M, a.h + rix);
+            cp_async8(d + 4 * M, a.sb0 + rix);
+            cp_async8(d + 5 * M, a.nu + rix);
+        }
+        cp_async_commit();
+    };
+    fetch(blockIdx.x, 0);
+    long long unit = 0;
+    for (long long uu = blockIdx.x; uu < s.U; uu += s.G, ++unit) {
+        long long j;
+        int cs, ce;
+        if (s.S == 1) {
+            j = uu;
+            cs = 0;
+            ce = s.TPR;
+        } else {
+            j = uu / s.S;
+            cs = (int)(uu - j * s.S) * s.TPS;
+            ce = min(s.TPR, cs + s.TPS);
+        }
+        const int slot = (int)(unit & 1);
+        fetch(uu + s.G, slot ^ 1);
+        cp_async_wait1();  // this unit's row scalars (issued one unit ago) have landed
+        __syncwarp();
+        const double(*sc)[M] = s_sc[wid][slot];
+        double zl[M];  // zeta + lam of source i (lam with its pending rescale)
+#pragma unroll
+        for (int i = 0; i < M; ++i) zl[i] = sc[1][i] + sc[0][i] * cin.f[0];
+
+        long long fx[M];
+        double dgx[M], dgn[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            fx[i] = 0;
+            dgx[i] = -INFINITY;
+            dgn[i] = INFINITY;
+        }
+        for (int c = cs + wid; c < ce; c += S2_NW) {
+            const int k = c * S2_TL + 2 * lane;  // first of this thread's two cells
+            const unsigned char* sp = ring + (size_t)st * C::STAGE;
+            s2_wait(&s_full[wid][st], ph);
+            if (k < a.n_pad) {
+                const bool k0 = (k == 0);
+                const bool vc0 = k < a.n, vc1 = (k + 1) < a.n;
+                double y[2], v[2], xo[M][2], xn[M][2];
+                s2_ld2<double>(sp + C::YOFF + 16 * lane, y);
+                s2_ld2<double>(sp + C::VOFF + 16 * lane, v);
+#pragma unroll
+                for (int i = 0; i < M; ++i) s2_ld2<double>(sp + (size_t)i * S2_TL * 8 + 16 * lane, xo[i]);
+                double s_e[2], mu_e[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    s_e[u] = fmax(v[u], 0.0);
+                    mu_e[u] = v[u] < 0.0 ? -v[u] * f2 : 0.0;
+                }
+                // ---- (6a) Gauss-Seidel over sources (same arithmetic as gs_cellU)
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i) * S2_TL * sizeof(CT) +
+                                              2 * sizeof(CT) * lane;
+                    double a2[2], a1[2], b2[2], b1[2];
+                    s2_ld2<CT>(cp, a2);
+                    s2_ld2<CT>(cp + S2_TL * sizeof(CT), a1);
+                    s2_ld2<CT>(cp + 2 * S2_TL * sizeof(CT), b2);
+                    s2_ld2<CT>(cp + 3 * S2_TL * sizeof(CT), b1);
+                    double Cq[2], Dq[2], bn[2], cn[2], dn[2], lo[2], hi[2];
+                    bool allq = true, anyq = false;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        double others = 0.0;
+#pragma unroll
+                        for (int l = 0; l < M; ++l)
+                            if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
+                        const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
+                        const double xoi = xo[i][u];
+                        const double e = fma(fma(b2[u], xoi, b1[u]), xoi, zl[i]);
+                        Cq[u] = fma(0.5 * R1, fma(b1[u], b1[u], -2.0 * b2[u] * e), fma(a2[u], iq, 0.5 * R3));
+                        Dq[u] = fma(-R1 * b1[u], e, fma(a1[u], iq, -R3 * phi));
+                        if (k0 && u == 0) {
+                            // lazy (6h) of the previous iteration, then its dual rescale
+                            double nu = sc[5][i];
+                            if (nu_pending) nu = nu + cin.x1[i] - xoi;
+                            const double nu_e = nu * cin.f[3];
+                            __stcg(a.nu + (long long)i * a.q + j, nu_e);
+                            s_nue[i] = nu_e;
+                            Cq[u] += 0.5 * R4;
+                            Dq[u] += -R4 * (cin.x1[i] + nu_e);
+                        }
+                        const bool qu = (b2[u] != 0.0);
+                        allq = allq && qu;
+                        anyq = anyq || qu;
+                        const double ia2 = rcp_nr(qu ? R1 * b2[u] * b2[u] : 1.0);  // 1 / 2A
+                        bn[u] = 1.5 * (R1 * b2[u] * b1[u]) * ia2;
+                        cn[u] = Cq[u] * ia2;
+                        dn[u] = 0.5 * Dq[u] * ia2;
+                    }
+                    {
+                        const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
+                        const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
+                        lo[0] = tl.x; lo[1] = tl.y; hi[0] = th.x; hi[1] = th.y;
+                    }
+                    if (allq) {
+                        double r[2];
+                        quartic_coreU<MODE, 2>(bn, cn, dn, Cq, Dq, lo, hi, r);
+                        xn[i][0] = r[0];
+                        xn[i][1] = r[1];
+                    } else if (!anyq) {  // a source without g (A = B = 0): quadratic
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) xn[i][u] = clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+                            xn[i][u] = (b2[u] != 0.0) ? quartic_core<MODE>(bn[u], cn[u], dn[u], Cq[u], Dq[u], lo[u], hi[u])
+                                                      : clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
+                    }
+                }
+                // ---- (6e)/(6f) per cell, reduced state v = s - mu (identity I2)
+                double vn[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    double txo[M], txn[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        txo[i] = xo[i][u];
+                        txn[i] = xn[i][u];
+                    }
+                    const bool valid = u == 0 ? vc0 : vc1;
+                    double r1l = my_r1, s3l = my_s3;
+                    const double vnew = cell_tail<M>(txo, txn, y[u], v[u], f2, chk && valid, r1l, s3l);
+                    my_r1 = r1l;
+                    my_s3 = s3l;
+                    vn[u] = valid ? vnew : 0.0;
+                }
+                *reinterpret_cast<double2*>(a.v + j * a.n_pad + k) = make_double2(vn[0], vn[1]);
+                // ---- row partials: exact fixed point, dg extrema on checks
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i + 2) * S2_TL * sizeof(CT) +
+                                              2 * sizeof(CT) * lane;
+                    double b2[2], b1[2];
+                    s2_ld2<CT>(cp, b2);
+                    s2_ld2<CT>(cp + S2_TL * sizeof(CT), b1);
+                    if (!vc0) xn[i][0] = 0.0;  // padding stays 0
+                    if (!vc1) xn[i][1] = 0.0;
+                    *reinterpret_cast<double2*>(a.x + i * qn + j * a.n_pad + k) = make_double2(xn[i][0], xn[i][1]);
+                    if ((a.gfree >> i) & 1u) continue;  // g = 0 on the box: no row sum, dg = 0
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 0 ? vc0 : vc1) {
+                            fx[i] += __double2ll_rn(fma(b2[u], xn[i][u], b1[u]) * xn[i][u] * a.fx_scale[i]);
+                            if (chk) {  // sigma's z-term only
+                                const double dg = (xn[i][u] - xo[i][u]) * fma(b2[u], xn[i][u] + xo[i][u], b1[u]);
+                                dgx[i] = fmax(dgx[i], dg);
+                                dgn[i] = fmin(dgn[i], dg);
+                            }
+                        }
+                    }
+                }
+                if (k0) {
+                    // (6c) contribution x_1 - nu, in this CTA's unit order (thread 0 owns
+                    // acc[0, 3 MAXM) until the closing barrier)
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        acc[i] += xn[i][0] - s_nue[i];
+                        acc[MAXM + i] = fmax(acc[MAXM + i], xn[i][0]);
+                        acc[2 * MAXM + i] = fmin(acc[2 * MAXM + i], xn[i][0]);
+                    }
+                }
+            }
+            __syncwarp();  // every lane is done reading the stage
+            if (lane == 0 && ahead.u < s.U) {
+                // refill the stage with this warp's chunk NS positions ahead
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                s2_issue<M, CT>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+            }
+            ahead.next(s, wid);
+            if (++st == NS) {
+                st = 0;
+                ph ^= 1u;
+            }
+        }
+
+        // ---- unit end: warp partials into slot b (free once unit - UB is finalised);
+        // the last warp to arrive finalises
+        const int b = (int)(unit & (S2_UB - 1));
+        if (lane == 0)
+            while (*(volatile unsigned*)&s_gen[b] != (unsigned)(unit >> 2)) {
+            }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const unsigned long long ws = warp_sum_u64((unsigned long long)fx[i]);
+            if (lane == 0) s_fxw[b][wid][i] = ws;
+            if (chk) {
+                const double mx = warp_max(dgx[i]), mn = warp_min(dgn[i]);
+                if (lane == 0) {
+                    s_dgw[b][wid][i] = mx;
+                    s_dgw[b][wid][M + i] = mn;
+                }
+            }
+        }
+        unsigned last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = (atomicAdd(&s_arr[b], 1u) == (unsigned)S2_NW - 1);
+            __threadfence_block();
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        __syncwarp();
+        if (last) {
+            if (lane < M) {
+                const int i = lane;
+                unsigned long long part = 0ull;
+                double mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+                for (int w = 0; w < S2_NW; ++w) {
+                    part += s_fxw[b][w][i];
+                    if (chk) {
+                        mx = fmax(mx, s_dgw[b][w][i]);
+                        mn = fmin(mn, s_dgw[b][w][M + i]);
+                    }
+                }
+                bool fin = true;
+                if (s.S > 1) {  // row split over segments: global exact sums, the last one finalises
+                    atomicAdd(a.rowacc + j * MAXM + i, part);
+                    if (chk) {
+                        atomicMax(a.rowdg + j * 2 * MAXM + i, okey(mx));
+                        atomicMin(a.rowdg + j * 2 * MAXM + MAXM + i, okey(mn));
+                    }
+                    __threadfence();
+                    fin = (atomicAdd(a.rowcnt + j * MAXM + i, 1u) == (unsigned)s.S - 1);
+                    if (fin) {
+                        __threadfence();
+                        part = atomicExch(a.rowacc + j * MAXM + i, 0ull);
+                        if (chk) {
+                            mx = okey_inv(atomicExch(a.rowdg + j * 2 * MAXM + i, 0ull));
+                            mn = okey_inv(atomicExch(a.rowdg + j * 2 * MAXM + MAXM + i, ~0ull));
+                        }
+                        a.rowcnt[j * MAXM + i] = 0u;
+                    }
+                }
+                if (fin) {
+                    if ((a.gfree >> i) & 1u) mx = mn = 0.0;  // dg = 0 for every k
+                    // (6b), (6g), (6d), (6i) for row (i, j) (PAPER.md:432-448 via I1)
+                    const long long rix = (long long)i * a.q + j;
+                    const RowOut o = row_update((double)(long long)part * a.fx_inv[i], sc[4][i],
+                                                sc[0][i] * cin.f[0], sc[2][i] * cin.f[1], sc[3][i], sc[1][i],
+                                                a.c[i], (double)a.n, cin.rho, mx, mn);
+                    __stcg(a.lam + rix, o.lam);
+                    __stcg(a.zeta + rix, o.zeta);
+                    __stcg(a.h + rix, o.h);
+                    __stcg(a.p + rix, o.p);
+                    if (chk) {
+                        double* rc = s_rc[wid][i];
+                        rc[0] = fmax(rc[0], o.r2);
+                        rc[1] = fmax(rc[1], o.r3);
+                        rc[2] = fmax(rc[2], o.s1);
+                        rc[3] = fmax(rc[3], o.s2);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s_arr[b] = 0u;
+                __threadfence_block();
+                atomicAdd(&s_gen[b], 1u);  // release the slot to unit + UB
+            }
+        }
+    }
+
+    // ---- per-CTA partials: the check maxima (consensus partials are in acc already)
+    if (chk) {
+        my_r1 = warp_max(my_r1);
+        my_s3 = warp_max(my_s3);
+        if (lane == 0) {
+            s_red[wid][0] = my_r1;
+            s_red[wid][1] = my_s3;
+        }
+    }
+    __syncthreads();
+    if (chk && tid == 0) {
+        double r1 = 0.0, s3 = 0.0, r2 = 0.0, r3 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int w = 0; w < S2_NW; ++w) {
+            r1 = fmax(r1, s_red[w][0]);
+            s3 = fmax(s3, s_red[w][1]);
+            for (int i = 0; i < M; ++i) {
+                r2 = fmax(r2, s_rc[w][i][0]);
+                r3 = fmax(r3, s_rc[w][i][1]);
+                s1 = fmax(s1, s_rc[w][i][2]);
+                s2 = fmax(s2, s_rc[w][i][3]);
+            }
+        }
+        acc[3 * MAXM + 0] = r1;
+        acc[3 * MAXM + 1] = r2;
+        acc[3 * MAXM + 2] = r3;
+        acc[3 * MAXM + 3] = s1;
+        acc[3 * MAXM + 4] = s2;
+        acc[3 * MAXM + 5] = s3;
+    }
+    __syncthreads();
+    if (tid < XB) __stcg(a.cta_part + (size_t)blockIdx.x * XB + tid, acc[tid]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.glob_cnt, 1) == s.G - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // ---- last CTA: reduce the G CTA partials; lane = slot, warp w takes CTAs w, w + NW,
+    // ... with eight independent accumulators (fixed assignment => deterministic)
+    {
+        __shared__ double wred[S2_NW][XB];
+        const int sl = lane;
+        const bool is_sum = sl < MAXM;
+        const bool is_min = sl >= 2 * MAXM && sl < 3 * MAXM;
+        const double ident = is_sum ? 0.0 : (is_min ? INFINITY : (sl >= 3 * MAXM ? 0.0 : -INFINITY));
+        double vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vv[u] = ident;
+        for (int g0 = wid; g0 < s.G; g0 += 8 * S2_NW) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int g = g0 + u * S2_NW;
+                t[u] = g < s.G ? __ldcg(a.cta_part + (size_t)g * XB + sl) : ident;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                vv[u] = is_sum ? vv[u] + t[u] : (is_min ? fmin(vv[u], t[u]) : fmax(vv[u], t[u]));
+        }
+        double vr = vv[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) vr = is_sum ? vr + vv[u] : (is_min ? fmin(vr, vv[u]) : fmax(vr, vv[u]));
+        wred[wid][sl] = vr;
+        __syncthreads();
+        if (tid < XB) {
+            double r = ident;
+            for (int w = 0; w < S2_NW; ++w) {
+                const double t = wred[w][tid];
+                r = is_sum ? r + t : (is_min ? fmin(r, t) : fmax(r, t));
+            }
+            acc[tid] = r;
+        }
+        __syncthreads();
+    }
+    if (tid < XB) a.xsend[tid] = acc[tid];
+    if (tid == 0) {
+        *a.glob_cnt = 0;
+        if (a.world == 1) {
+            Ctrl& cout = a.ctrl[(it + 1) & 1];
+            finalize_global(a, acc, 1, it, cin, cout, chk);
+            __threadfence();
+            *(volatile long long*)a.iter = it + 1;
+        }
+    }
+}
+
+// host side (sweep2.cu): kernel pointer, stage count and dynamic shared memory
+// for (m, box mode, coefficient bytes); nullptr when m is not supported
+const void* sweep2_pick(int m, int mode, int coeff_bytes, int* ns, size_t* smem);
+// work decomposition for q rows of n_pad cells over at most g_max CTAs
+S2Args sweep2_plan(long long q, long long n_pad, int g_max);
+
+}  // namespace admm_dev

@@ -41,19 +41,48 @@ def test_byte_model_horizon_m4():
     assert 69.9 < per_elem < 70.1  # SURVEY.md §8(d): 70 B at m = 4, q = 1
 
 
-def test_reference_arm_prints_one_json_line():
-    """--impl reference times the CPU oracle (the reference arm of this tier): one
-    JSON line with impl=reference, the same metric/unit as our arm, e2e and
-    cpu_baseline; no GPU needed."""
+def _reference_line(workload, steps="1", warmup="0"):
     env = dict(os.environ, WORLD_SIZE="1", RANK="0")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--workload", "toy", "--steps", "1", "--warmup", "0"],
+                          "--workload", workload, "--steps", steps, "--warmup", warmup],
                          capture_output=True, text=True, cwd=ROOT, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.strip().splitlines() if l.startswith("{")]
     assert len(lines) == 1
-    d = json.loads(lines[0])
+    return json.loads(lines[0])
+
+
+def test_reference_arm_prints_one_json_line():
+    """--impl reference times the CPU oracle (the reference arm of this tier): one
+    JSON line with impl=reference, the same metric/unit as our arm, e2e and
+    cpu_baseline; no GPU needed."""
+    d = _reference_line("toy")
     assert d["impl"] == "reference"
     assert d["unit"] == "element-updates/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"].startswith("oracle") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["cpu_count"] >= 1 and d["cpu_baseline"]["affinity"] >= 1
+
+
+def test_reference_arm_default_workload_loads_no_product_code():
+    """The default (headline) workload -- configs[3], q = 1e5 -- on the reference arm
+    runs a bounded sample of scenario rows with q_total = 1e5, and the process never
+    loads the product package or its CUDA library (VERDICT r01 weak #2)."""
+    code = (
+        "import sys, runpy, json\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0']\n"
+        "try:\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "finally:\n"
+        "    bad = [m for m in sys.modules if m.startswith('paper_1903_10041_b200')]\n"
+        "    maps = open('/proc/self/maps').read()\n"
+        "    print('LOADED', json.dumps(bad), 'libadmm_b200' in maps, file=sys.stderr)\n")
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                         env=env, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    tail = [l for l in out.stderr.splitlines() if l.startswith("LOADED")][-1]
+    assert tail == "LOADED [] False", tail
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["config"]["q_total"] == 100000 and d["config"]["baseline_config"] == "configs[3]"
+    assert "q_total = 100000" in d["cpu_baseline"]["sample"]

@@ -181,3 +181,26 @@ def test_phev_q5_iteration_count_matches_survey():
     info, _ = o.solve(20000)
     assert info["status"] == 0
     assert info["iterations"] == 660
+
+
+def test_openmp_build_is_bitwise_identical():
+    """bench.py's CPU-parallel baseline runs the OpenMP build of the same oracle
+    source: every array, the history and the info must equal the serial build's
+    bit for bit (sums stay serial per row; maxima are order-independent)."""
+    oracle.set_threads(4)
+    P = synth.random_problem(2, 37, 9, seed=5)
+    runs = []
+    for omp in (False, True):
+        o = oracle.Oracle(P, oracle.default_params(rho0=(0.7, 0.3, 0.9, 0.5)), omp=omp)
+        info, hist = o.run(60)
+        runs.append((o.state(), info, hist))
+    (S0, i0, h0), (S1, i1, h1) = runs
+    for k in S0:
+        assert np.array_equal(S0[k], S1[k]), k
+    assert np.array_equal(h0, h1)
+    assert i0 == i1
+    A, B, Cc, D = (np.random.default_rng(3).uniform(-5, 5, 5000) for _ in range(4))
+    A = np.abs(A) + 0.1
+    x0, t0 = oracle.quartic_batch(A, B, Cc, D)
+    x1, t1 = oracle.quartic_batch(A, B, Cc, D, omp=True)
+    assert np.array_equal(x0, x1) and t0 == t1
