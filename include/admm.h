@@ -89,13 +89,30 @@ typedef enum {
     ADMM_ENGINE_STREAM_TMA = 4   /* sweep2_kernel: TMA-fed streaming sweep, one launch per iteration (default for finite boxes) */
 } admm_engine;
 
-/* Scenario sharding across ranks (one process per GPU).  Rank r owns the
-   scenarios j in [j_begin, j_end) of q_total.  nccl_id comes from
-   admm_nccl_unique_id on rank 0, broadcast by the caller (torch.distributed). */
+/* Multi-GPU partition (one process per GPU; the method is
+   "parallel for k and j").  nccl_id comes from admm_nccl_unique_id
+   on rank 0, broadcast by the caller (torch.distributed).  A non-NULL admm_dist
+   always runs the collective path, also at world = 1 (a one-rank communicator:
+   the same graph, exchanges and finalisation as world > 1).
+   mode = ADMM_SHARD_SCENARIOS: rank r owns the scenarios j in [j_begin, j_end) of
+     q_total and every step; per iteration the ranks all-gather 32 doubles
+     (consensus sums of (6c), residual maxima).  k_begin / k_end are ignored.
+   mode = ADMM_SHARD_HORIZON: rank r owns the steps k in [k_begin, k_end) of the
+     n-step horizon and every scenario (j_begin = 0, j_end = q_total); the
+     per-row sums over k of (6b)/(6d) (exact 64-bit fixed point, m q values)
+     and their dg extrema are all-reduced every iteration, every rank finalises
+     every row identically, and the rank with k_begin = 0 owns the consensus
+     cell k = 1 (horizon length must not grow the time per
+     iteration).  Needs finite boxes; the problem arrays passed to
+     admm_set_problem are the rank's [k_begin, k_end) slices. */
+typedef enum { ADMM_SHARD_SCENARIOS = 0, ADMM_SHARD_HORIZON = 1 } admm_shard_mode;
 typedef struct {
     int32_t rank, world;
     int64_t j_begin, j_end;
     unsigned char nccl_id[128];
+    int64_t k_begin, k_end;  /* ADMM_SHARD_HORIZON only */
+    int32_t mode;            /* admm_shard_mode */
+    int32_t reserved;
 } admm_dist;
 
 /* Parameters; admm_default_params() fills the paper's values (PAPER.md:317-324,

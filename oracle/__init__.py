@@ -49,7 +49,7 @@ class _Problem(C.Structure):
     _fields_ = [("m", C.c_int), ("n", C.c_long), ("q", C.c_long), ("q_total", C.c_long)] + [
         (nm, C.POINTER(C.c_double))
         for nm in ("a2", "a1", "a0", "b2", "b1", "b0", "lo", "hi", "y", "c")
-    ]
+    ] + [("n_total", C.c_long), ("k_off", C.c_long)]
 
 
 class _State(C.Structure):
@@ -174,9 +174,11 @@ class Oracle:
     prob: dict from synth (m, n, q, a2.., lo, hi, y, c).  q_total defaults to
     prob['q'].  reduce: optional python callable reduce(np_array, op) that
     all-reduces in place (op 0 = sum, 1 = max) -- used by the gloo tests.
-    omp: run on the OpenMP build (bitwise-identical results, CPU-parallel baseline)."""
+    omp: run on the OpenMP build (bitwise-identical results, CPU-parallel baseline).
+    horizon=(n_total, k_off): this process holds steps [k_off, k_off + n) of an
+    n_total-step horizon (horizon-block sharding; row sums over k go through reduce)."""
 
-    def __init__(self, prob, params=None, q_total=None, reduce=None, omp=False):
+    def __init__(self, prob, params=None, q_total=None, reduce=None, omp=False, horizon=None):
         self._lib = lib(omp)
         self.prob = {k: (_f64(v) if isinstance(v, np.ndarray) else v) for k, v in prob.items()}
         P = self.prob
@@ -184,9 +186,10 @@ class Oracle:
         self.m, self.n, self.q = m, n, q
         self.q_total = int(q_total if q_total is not None else q)
         self.params = default_params() if params is None else dict(params)
+        n_total, k_off = horizon if horizon is not None else (0, 0)
         self._P = _Problem(m, n, q, self.q_total,
                            *[_p(P[k]) for k in ("a2", "a1", "a0", "b2", "b1", "b0", "lo",
-                                                "hi", "y", "c")])
+                                                "hi", "y", "c")], int(n_total), int(k_off))
         self.x = np.zeros((m, q, n)); self.z = np.zeros((m, q, n)); self.lam = np.zeros((m, q, n))
         self.s = np.zeros((q, n)); self.mu = np.zeros((q, n))
         self.h = np.zeros((m, q)); self.p = np.zeros((m, q)); self.nu = np.zeros((m, q))

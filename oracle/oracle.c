@@ -353,18 +353,28 @@ void orc_init(const orc_problem *P, orc_state *S, const orc_params *prm,
             S->s[JK(j, k)] = fmax(0.0, sx - P->y[JK(j, k)]);
             S->mu[JK(j, k)] = 0.0;
         }
+    const int hz = P->n_total > 0;       /* horizon-sharded */
+    const int own_k1 = !hz || P->k_off == 0; /* this process holds the k = 1 cell */
+    double *rs = (double *)calloc((size_t)m * q, sizeof(double));
     for (int i = 0; i < m; ++i)
         for (long j = 0; j < q; ++j) {
             nsum a = {0, 0};
             for (long k = 0; k < n; ++k) nsum_add(&a, S->z[IX(i, j, k)]);
-            S->h[IJ(i, j)] = fmin(P->c[i], nsum_val(&a));
+            rs[IJ(i, j)] = nsum_val(&a);
+        }
+    if (hz) reduce(rfn, user, rs, (int)(m * q), 0); /* 1'z over the horizon blocks */
+    for (int i = 0; i < m; ++i)
+        for (long j = 0; j < q; ++j) {
+            S->h[IJ(i, j)] = fmin(P->c[i], rs[IJ(i, j)]);
             S->p[IJ(i, j)] = 0.0;
             S->nu[IJ(i, j)] = 0.0;
         }
+    free(rs);
     double *buf = (double *)calloc((size_t)m, sizeof(double));
     for (int i = 0; i < m; ++i) {
         nsum a = {0, 0};
-        for (long j = 0; j < q; ++j) nsum_add(&a, S->x[IX(i, j, 0)]);
+        if (own_k1)
+            for (long j = 0; j < q; ++j) nsum_add(&a, S->x[IX(i, j, 0)]);
         buf[i] = nsum_val(&a);
     }
     reduce(rfn, user, buf, m, 0);
@@ -406,6 +416,9 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
     double *W = (double *)malloc(NR * sizeof(double));
     double *sz = (double *)malloc(NR * sizeof(double));  /* 1'z */
     double *buf = (double *)malloc((size_t)(m + 8) * sizeof(double));
+    const int hz = P->n_total > 0;                 /* horizon-sharded */
+    const int own_k1 = !hz || P->k_off == 0;       /* this process holds the k = 1 cell */
+    const double nd = hz ? (double)P->n_total : (double)n; /* horizon length in (6b) */
     int status = ORC_NOT_CONVERGED;
     long ties = 0, rows = 0, done = 0;
     double r = NAN, sigma = NAN;
@@ -434,7 +447,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                     double phi = S->s[JK(j, k)] - others + P->y[JK(j, k)] + S->mu[JK(j, k)];
                     double cf[4];
                     orc_build_quartic(P->a2[e], P->a1[e], P->b2[e], P->b1[e], P->b0[e], theta,
-                                      phi, qd, rho, k == 0, S->x1[i], S->nu[IJ(i, j)], cf);
+                                      phi, qd, rho, own_k1 && k == 0, S->x1[i], S->nu[IJ(i, j)], cf);
                     int tie = 0;
                     S->x[e] = orc_quartic_boxmin(cf[0], cf[1], cf[2], cf[3], P->lo[IK(i, k)],
                                                  P->hi[IK(i, k)], prm->box_mode, &tie);
@@ -443,7 +456,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
 
         /* (6b) PAPER.md:431-434: z = w + rho2/(rho1 + n rho2) 1 (h + p - 1'w),
            w = g(x) - lambda */
-        double kap = rho[1] / (rho[0] + (double)n * rho[1]);
+        double kap = rho[1] / (rho[0] + nd * rho[1]);
 #pragma omp parallel for collapse(2) schedule(static)
         for (int i = 0; i < m; ++i)
             for (long j = 0; j < q; ++j) {
@@ -453,6 +466,11 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                     nsum_add(&a, gfun(P, e, S->x[e]) - S->lam[e]);
                 }
                 W[IJ(i, j)] = nsum_val(&a);
+            }
+        if (hz) reduce(rfn, user, W, (int)NR, 0); /* 1'w over the horizon blocks */
+#pragma omp parallel for collapse(2) schedule(static)
+        for (int i = 0; i < m; ++i)
+            for (long j = 0; j < q; ++j) {
                 double corr = kap * (S->h[IJ(i, j)] + S->p[IJ(i, j)] - W[IJ(i, j)]);
                 for (long k = 0; k < n; ++k) {
                     long e = IX(i, j, k);
@@ -465,7 +483,8 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
            before (6h).  The sum over j crosses shards: rfn (sum). */
         for (int i = 0; i < m; ++i) {
             nsum a = {0, 0};
-            for (long j = 0; j < q; ++j) nsum_add(&a, S->x[IX(i, j, 0)] - S->nu[IJ(i, j)]);
+            if (own_k1)
+                for (long j = 0; j < q; ++j) nsum_add(&a, S->x[IX(i, j, 0)] - S->nu[IJ(i, j)]);
             buf[i] = nsum_val(&a);
         }
         reduce(rfn, user, buf, m, 0);
@@ -478,8 +497,11 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
                 nsum a = {0, 0};
                 for (long k = 0; k < n; ++k) nsum_add(&a, S->z[IX(i, j, k)]);
                 sz[IJ(i, j)] = nsum_val(&a);
-                S->h[IJ(i, j)] = fmin(P->c[i], sz[IJ(i, j)] - S->p[IJ(i, j)]);
             }
+        if (hz) reduce(rfn, user, sz, (int)NR, 0); /* 1'z over the horizon blocks */
+        for (int i = 0; i < m; ++i)
+            for (long j = 0; j < q; ++j)
+                S->h[IJ(i, j)] = fmin(P->c[i], sz[IJ(i, j)] - S->p[IJ(i, j)]);
 
         /* (6e) PAPER.md:440: s = max(0, sum_i x - y - mu);
            (6f) PAPER.md:442: mu = mu + s - sum_i x + y */
@@ -503,9 +525,10 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
 #pragma omp parallel for schedule(static)
         for (size_t e = 0; e < NE; ++e) S->lam[e] = S->lam[e] + S->z[e] - gfun(P, (long)e, S->x[e]);
         /* (6h) PAPER.md:446: nu = nu + x1 - x_1^{(i,j)} */
-        for (int i = 0; i < m; ++i)
-            for (long j = 0; j < q; ++j)
-                S->nu[IJ(i, j)] = S->nu[IJ(i, j)] + S->x1[i] - S->x[IX(i, j, 0)];
+        if (own_k1)
+            for (int i = 0; i < m; ++i)
+                for (long j = 0; j < q; ++j)
+                    S->nu[IJ(i, j)] = S->nu[IJ(i, j)] + S->x1[i] - S->x[IX(i, j, 0)];
         /* (6i) PAPER.md:448: p = p + h - 1'z (1'z after (6b)) */
         for (int i = 0; i < m; ++i)
             for (long j = 0; j < q; ++j)
@@ -544,7 +567,7 @@ int orc_run(const orc_problem *P, orc_state *S, const orc_params *prm, long iter
             for (int i = 0; i < m; ++i)
                 for (long j = 0; j < q; ++j) {
                     t[2] = fmax(t[2], fabs(S->h[IJ(i, j)] - sz[IJ(i, j)]));
-                    t[3] = fmax(t[3], fabs(S->x[IX(i, j, 0)] - S->x1[i]));
+                    if (own_k1) t[3] = fmax(t[3], fabs(S->x[IX(i, j, 0)] - S->x1[i]));
                     t[5] = fmax(t[5], fabs(S->h[IJ(i, j)] - ht[IJ(i, j)]));
                 }
             reduce(rfn, user, t, 7, 1);

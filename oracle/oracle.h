@@ -42,6 +42,13 @@ typedef struct {
     const double *lo, *hi;
     const double *y;
     const double *c;
+    /* horizon-block sharding ("in parallel for k and
+       j"): this process holds steps [k_off, k_off + n) of an n_total-step horizon
+       and every scenario; the per-row sums over k ((6b) 1'w, (6d) 1'z, the
+       initial 1'z) are summed over the processes with the reduce callback, and
+       only the process with k_off = 0 owns the k = 1 consensus cell.
+       n_total = 0: unsharded horizon (n_total = n, k_off = 0). */
+    long n_total, k_off;
 } orc_problem;
 
 typedef struct {

@@ -34,5 +34,5 @@ from ._lib import (  # noqa: F401
     admm_solve,
     admm_workspace_bytes,
 )
-from .dist import make_dist, shard_range  # noqa: F401
+from .dist import dist_for, horizon_range, make_dist, shard_range  # noqa: F401
 from .solver import AdmmSolver, quartic_minimize_batch  # noqa: F401

@@ -33,9 +33,13 @@ STATUS_NAMES = {0: "ADMM_OK", 1: "ADMM_ERR_INVALID", 2: "ADMM_NOT_CONVERGED",
                 6: "ADMM_ERR_NCCL", 7: "ADMM_ERR_STATE"}
 
 
+ADMM_SHARD_SCENARIOS, ADMM_SHARD_HORIZON = 0, 1
+
+
 class admm_dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("j_begin", C.c_int64),
-                ("j_end", C.c_int64), ("nccl_id", C.c_ubyte * 128)]
+                ("j_end", C.c_int64), ("nccl_id", C.c_ubyte * 128), ("k_begin", C.c_int64),
+                ("k_end", C.c_int64), ("mode", C.c_int32), ("reserved", C.c_int32)]
 
 
 class admm_params(C.Structure):

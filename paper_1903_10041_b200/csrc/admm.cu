@@ -7,9 +7,11 @@
 //     check_every sweep launches; the last CTA of each sweep sets the
 //     condition (not done and iteration limit not reached), so a whole solve
 //     runs with zero host round trips;
-//   * multi-GPU (world > 1): the body is check_every x [sweep ->
-//     ncclAllGather(per-rank aggregates, 32 doubles) -> finalize_kernel],
-//     driven by a host loop that polls the done flag once per body.
+//   * multi-GPU (an admm_dist given, any world size): the body is check_every x
+//     [sweep -> ncclAllGather(per-rank aggregates, 32 doubles) -> finalize_kernel]
+//     (scenario sharding) or [sweep -> ncclAllReduce(row sums, dg extrema) ->
+//     ncclAllGather -> hz_rows_kernel] (horizon blocks), driven by a host loop
+//     that polls the done flag once per body.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -40,7 +42,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, cf, total;
+        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, cf, hzdg, hzrow, total;
 };
 
 // streaming sweep block size: 2 cells per thread, at most ADMM_SWEEP_BS (default
@@ -101,6 +103,8 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.rowdg = take((size_t)q * 2 * MAXM * 8);
     L.rowcnt = take((size_t)q * MAXM * 4);
     L.cf = take(2 * E);  // F2: fp32 a2, a1, b2, b1 [4][m][q][n_pad] (16 B per element)
+    L.hzdg = take((size_t)q * 2 * MAXM * 8);  // horizon blocks: dg extrema keys per row
+    L.hzrow = take((size_t)2 * m * q * 8);     // initial row sums (all-reduced over horizon blocks)
     L.total = o;
     return L;
 }
@@ -223,8 +227,9 @@ __device__ double block_sum_256(double v, double* sh) {
     return r;  // valid in threads < 32
 }
 
-// per row (i,j): sb0 = sum_k b0; h = min(c, sum_k g(x)); lam = zeta = p = nu = 0
-__global__ void __launch_bounds__(256) init_rows_kernel(KArgs a) {
+// per row (i,j): this rank's sum_k g(x) and sum_k b0 (all-reduced over horizon blocks),
+// then sb0 = sum_k b0; h = min(c, sum_k g(x)); lam = zeta = p = nu = 0
+__global__ void __launch_bounds__(256) init_rows_kernel(KArgs a, double* rs) {
     __shared__ double sh[8];
     const long long rix = blockIdx.x;  // i * q + j
     const int i = (int)(rix / a.q);
@@ -241,8 +246,19 @@ __global__ void __launch_bounds__(256) init_rows_kernel(KArgs a) {
     sg = block_sum_256(sg, sh);
     s0 = block_sum_256(s0, sh);
     if (threadIdx.x == 0) {
-        ((double*)a.sb0)[rix] = s0;
-        a.h[rix] = fmin(a.c[i], sg);
+        rs[rix] = sg;
+        rs[(long long)a.m * a.q + rix] = s0;
+    }
+    (void)i;
+}
+
+__global__ void init_rows_fin_kernel(KArgs a, const double* rs) {
+    const long long R = (long long)a.m * a.q;
+    for (long long rix = blockIdx.x * (long long)blockDim.x + threadIdx.x; rix < R;
+         rix += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(rix / a.q);
+        ((double*)a.sb0)[rix] = rs[R + rix];
+        a.h[rix] = fmin(a.c[i], rs[rix]);
         a.lam[rix] = 0.0;
         a.zeta[rix] = 0.0;
         a.p[rix] = 0.0;
@@ -250,12 +266,13 @@ __global__ void __launch_bounds__(256) init_rows_kernel(KArgs a) {
     }
 }
 
-// consensus partial sums sum_j x_1^{(i,j)} - nu (fixed order) -> xsend
+// consensus partial sums sum_j x_1^{(i,j)} - nu (fixed order) -> xsend; zero on a rank
+// without the k = 1 cell (horizon blocks)
 __global__ void cons_partial_kernel(KArgs a, int with_nu) {
     if (threadIdx.x >= 32) return;
     for (int i = 0; i < a.m; ++i) {
         double s = 0.0;
-        for (long long j = threadIdx.x; j < a.q; j += 32) {
+        for (long long j = threadIdx.x; a.k0own && j < a.q; j += 32) {
             const long long rix = (long long)i * a.q + j;
             s += a.x[rix * a.n_pad] - (with_nu ? a.nu[rix] : 0.0);
         }
@@ -458,6 +475,9 @@ struct admm_ctx {
     cudaStream_t stream = nullptr;      // caller's stream: all work is ordered on it
     cudaStream_t cap_stream = nullptr;  // private stream used only to capture the graph
     int world = 1, rank = 0;
+    bool dist = false;            // collective path (admm_dist given, any world size)
+    bool hz = false;              // horizon-block sharding (ADMM_SHARD_HORIZON)
+    long long n_total = 0, k_begin = 0;  // whole horizon, this rank's first step (hz)
     ncclComm_t comm = nullptr;
     bool owns_ws = false;
     char* ws = nullptr;
@@ -677,9 +697,18 @@ admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
         } else
             fn<<<ctx->G, ctx->bs, pf_smem_bytes(ctx), st>>>(ctx->ka);
         CKC(cudaGetLastError());
-        if (ctx->world > 1) {
+        if (ctx->dist) {
+            if (ctx->hz) {  // row sums over k and their dg extrema, every rank's rows
+                CKN(ncclAllReduce(ctx->ka.rowacc, ctx->ka.rowacc, (size_t)ctx->q * MAXM, ncclUint64, ncclSum,
+                                  ctx->comm, st));
+                CKN(ncclAllReduce(ctx->ka.hzdg, ctx->ka.hzdg, (size_t)ctx->q * 2 * MAXM, ncclUint64, ncclMax,
+                                  ctx->comm, st));
+            }
             CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, st));
-            finalize_kernel<<<1, 32, 0, st>>>(ctx->ka);
+            if (ctx->hz)
+                hz_rows_kernel<<<1, 256, 0, st>>>(ctx->ka);
+            else
+                finalize_kernel<<<1, 32, 0, st>>>(ctx->ka);
             CKC(cudaGetLastError());
         }
     }
@@ -718,7 +747,7 @@ admm_status build_graph(admm_ctx* ctx) {
         admm_status ps = plan_stream(ctx);
         if (ps != ADMM_OK) return ps;
     }
-    if (ctx->world == 1) {
+    if (!ctx->dist) {
         CKC(cudaGraphCreate(&ctx->graph, 0));
         cudaGraphConditionalHandle h;
         CKC(cudaGraphConditionalHandleCreate(&h, ctx->graph, 1, cudaGraphCondAssignDefault));
@@ -782,7 +811,7 @@ struct PPlan {
 // state fits in shared memory; all CTAs must be co-resident
 PPlan plan_persist(admm_ctx* ctx, persist_fn fn) {
     PPlan pl;
-    if (ctx->world > 1 || !fn) return pl;
+    if (ctx->dist || !fn) return pl;
     const long long n = ctx->n, q = ctx->q;
     const int sms = ctx->sms;
     long long T = std::max<long long>((n + 1023) / 1024, q <= sms ? sms / q : 1);
@@ -857,7 +886,7 @@ cluster_fn pick_cluster(int m, int mode) {
 // long row does not fit the shared memory of T CTAs).
 PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     PPlan pl;
-    if (ctx->world > 1 || !fn || !ctx->prep_ok || !ctx->fx_ok) return pl;
+    if (ctx->dist || !fn || !ctx->prep_ok || !ctx->fx_ok) return pl;
     const long long n = ctx->n, q = ctx->q;
     const int sms = ctx->sms;
     if (q > 32LL * sms) return pl;
@@ -982,6 +1011,9 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     if (!pl.ok && !cpl.ok) {
         st = build_graph(ctx);
         if (st != ADMM_OK) return st;
+        if (ctx->hz && !ctx->use_tma)
+            return fail(ctx, ADMM_ERR_INVALID,
+                        "horizon blocks need the TMA sweep: finite boxes and m <= 4");
     }
     ctx->last_engine = cpl.ok ? ADMM_ENGINE_CLUSTER
                               : (pl.ok ? ADMM_ENGINE_GRID
@@ -1004,12 +1036,12 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         while (true) {
             st = record_body(ctx, fn, ctx->stream);
             if (st != ADMM_OK) return st;
-            ctx->launches += (long long)std::max(1, ctx->params.check_every) * (ctx->world > 1 ? 2 : 1);
+            ctx->launches += (long long)std::max(1, ctx->params.check_every) * (ctx->dist ? 2 : 1);
             st = read_ctrl(ctx);
             if (st != ADMM_OK) return st;
             if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
         }
-    } else if (ctx->world == 1) {
+    } else if (!ctx->dist) {
         CKC(cudaGraphLaunch(ctx->gexec, ctx->stream));
         graph_bodies = -1;  // counted after the call from the iterations done
     } else {
@@ -1034,7 +1066,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     {
         const long long K = std::max(1, ctx->params.check_every);
         if (graph_bodies < 0) graph_bodies = std::max(1LL, (did + K - 1) / K);  // while-node passes
-        ctx->launches += graph_bodies * (K * (ctx->world > 1 ? 2 : 1) + (ctx->world > 1 ? 0 : 1));
+        ctx->launches += graph_bodies * (K * (ctx->dist ? 2 : 1) + (ctx->dist ? 0 : 1));
     }
     if (ctx->h_ctrl->err) return fail(ctx, ADMM_ERR_NUMERICAL, "NaN/Inf in residuals");
     return ADMM_OK;
@@ -1057,7 +1089,7 @@ admm_status compute_objective(admm_ctx* ctx, double* out) {
     ctx->launches += 2;
     CKC(cudaGetLastError());
     double tot = 0.0;
-    if (ctx->world > 1) {
+    if (ctx->dist) {
         CKN(ncclAllGather(ctx->ka.xsend, ctx->ka.xall, XB, ncclDouble, ctx->comm, ctx->stream));
         std::vector<double> all((size_t)ctx->world * XB);
         CKC(cudaMemcpyAsync(all.data(), ctx->ka.xall, all.size() * 8, cudaMemcpyDeviceToHost,
@@ -1097,15 +1129,19 @@ admm_status init_state(admm_ctx* ctx) {
     KArgs& a = ctx->ka;
     const long long R = (long long)ctx->m * ctx->q;
     init_cells_kernel<<<grid_for(ctx->q * ctx->n_pad, 256, ctx->sms), 256, 0, ctx->stream>>>(a);
-    init_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(a);
+    double* rs = (double*)(ctx->ws + ctx->L.hzrow);  // [2][m][q]: sum_k g(x), sum_k b0
+    init_rows_kernel<<<(unsigned)R, 256, 0, ctx->stream>>>(a, rs);
+    CKC(cudaGetLastError());
+    if (ctx->hz) CKN(ncclAllReduce(rs, rs, (size_t)2 * R, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    init_rows_fin_kernel<<<grid_for(R, 256, ctx->sms), 256, 0, ctx->stream>>>(a, rs);
     cons_partial_kernel<<<1, 32, 0, ctx->stream>>>(a, 0);
     CKC(cudaGetLastError());
     const double* agg = a.xsend;
-    if (ctx->world > 1) {
+    if (ctx->dist) {
         CKN(ncclAllGather(a.xsend, a.xall, XB, ncclDouble, ctx->comm, ctx->stream));
         agg = a.xall;
     }
-    ctx->launches += 4;  // init_cells, init_rows, cons_partial, init_ctrl
+    ctx->launches += 5;  // init_cells, init_rows, init_rows_fin, cons_partial, init_ctrl
     init_ctrl_kernel<<<1, 32, 0, ctx->stream>>>(a, agg, ctx->world, ctx->params.rho[0],
                                                  ctx->params.rho[1], ctx->params.rho[2],
                                                  ctx->params.rho[3]);
@@ -1164,21 +1200,36 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     admm_ctx* ctx = new admm_ctx();
     ctx->m = m;
     ctx->n = n;
-    ctx->n_pad = (long long)align_up((size_t)n, 4);
+    ctx->n_total = n;
     ctx->q_total = q_total;
     ctx->q = q_total;
     ctx->device = device;
-    if (dist && dist->world > 1) {
-        if (dist->rank < 0 || dist->rank >= dist->world || dist->world > MAX_WORLD ||
-            dist->j_begin < 0 || dist->j_end <= dist->j_begin || dist->j_end > q_total) {
+    if (dist) {
+        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || dist->world > MAX_WORLD ||
+            dist->j_begin < 0 || dist->j_end <= dist->j_begin || dist->j_end > q_total ||
+            (dist->mode != ADMM_SHARD_SCENARIOS && dist->mode != ADMM_SHARD_HORIZON)) {
             delete ctx;
             return ADMM_ERR_INVALID;
         }
+        ctx->dist = true;
         ctx->world = dist->world;
         ctx->rank = dist->rank;
         ctx->j0 = dist->j_begin;
         ctx->q = dist->j_end - dist->j_begin;
+        if (dist->mode == ADMM_SHARD_HORIZON) {
+            // every scenario, steps [k_begin, k_end) of the horizon
+            if (dist->j_begin != 0 || dist->j_end != q_total || dist->k_begin < 0 ||
+                dist->k_end <= dist->k_begin || dist->k_end > n) {
+                delete ctx;
+                return ADMM_ERR_INVALID;
+            }
+            ctx->hz = true;
+            ctx->k_begin = dist->k_begin;
+            ctx->n = dist->k_end - dist->k_begin;
+        }
     }
+    ctx->n_pad = (long long)align_up((size_t)ctx->n, 4);
+    n = ctx->n;  // local horizon from here on
     admm_status st = ADMM_OK;
     auto bail = [&](admm_status s) {
         *out = ctx;  // keep ctx so the caller can read admm_last_error, then destroy it
@@ -1243,6 +1294,10 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     a.G = 1;
     a.world = ctx->world;
     a.rank = ctx->rank;
+    a.dist = ctx->dist ? 1 : 0;
+    a.hz = ctx->hz ? 1 : 0;
+    a.k0own = (!ctx->hz || ctx->k_begin == 0) ? 1 : 0;
+    a.nd = (double)ctx->n_total;
     a.q = ctx->q;
     a.q_total = q_total;
     a.inv_q = 1.0 / (double)q_total;
@@ -1263,6 +1318,7 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     a.rowacc = (unsigned long long*)(w + L.rowacc);
     a.rowdg = (unsigned long long*)(w + L.rowdg);
     a.rowcnt = (unsigned*)(w + L.rowcnt);
+    a.hzdg = (unsigned long long*)(w + L.hzdg);
     {
         const size_t NE = (size_t)m * ctx->q * ctx->n_pad;
         float* cf = (float*)(w + L.cf);
@@ -1270,7 +1326,7 @@ admm_status admm_create(admm_ctx** out, int32_t m, int64_t n, int64_t q_total, c
     }
     ctx->vflag = (unsigned long long*)(w + L.vflag);
     ctx->obj_rows = (double*)(w + L.obj_rows);
-    if (ctx->world > 1) {
+    if (ctx->dist) {
         ncclUniqueId id;
         memcpy(id.internal, dist->nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
@@ -1348,6 +1404,9 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
         gbound_kernel<<<grid_for(blk, 256, ctx->sms), 256, 0, ctx->stream>>>(
             ctx->m, ctx->q, ctx->n, ctx->n_pad, a.b2, a.b1, a.lo, a.hi, gb);
         CKC(cudaGetLastError());
+        // one fixed-point scale per source on every rank (horizon blocks: the bound of
+        // the whole row; scenario shards: identical scales keep the sums exact alike)
+        if (ctx->dist) CKN(ncclAllReduce(gb, gb, MAXM, ncclUint64, ncclMax, ctx->comm, ctx->stream));
         rowdg_init_kernel<<<grid_for(ctx->q * 2 * MAXM, 256, ctx->sms), 256, 0, ctx->stream>>>(
             (unsigned long long*)(ctx->ws + ctx->L.rowdg), ctx->q);
         CKC(cudaGetLastError());
@@ -1361,7 +1420,7 @@ admm_status admm_set_problem(admm_ctx* ctx, const double* f, const double* g, co
             unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
             double gbv;
             std::memcpy(&gbv, &u, 8);
-            const double G = (double)ctx->n * gbv;  // bound on |sum_k (b2 x^2 + b1 x)|
+            const double G = (double)ctx->n_total * gbv;  // bound on |sum_k (b2 x^2 + b1 x)|
             if (!(G < 1e300)) {
                 ok = false;
                 break;

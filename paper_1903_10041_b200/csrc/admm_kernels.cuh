@@ -55,6 +55,10 @@ struct DParams {
 
 struct KArgs {
     int m, n, n_pad, T, tile, G, world, rank;
+    int dist;   // collective path (admm_dist given): kernels write xsend, finalize_kernel finishes
+    int hz;     // horizon-block sharding: row sums are all-reduced, hz_rows_kernel finalises rows
+    int k0own;  // this rank holds the consensus cell k = 1 (global k = 0)
+    double nd;  // horizon length n of the whole problem (row length in (6b), kappa)
     long long q, q_total;
     double inv_q;
     // problem (padded SoA)
@@ -84,6 +88,7 @@ struct KArgs {
     unsigned long long *rowacc;  // [q][MAXM]
     unsigned long long *rowdg;   // [q][2 MAXM] ordered keys (checks)
     unsigned *rowcnt;            // [q][MAXM]
+    unsigned long long *hzdg;    // [q][2 MAXM] horizon mode: max keys of dg, of -dg (zero between uses)
     unsigned gfree;              // bit i: g^{(i)} = 0 on the box (row sums 0, no capacity bookkeeping)
     // F2: fp32 copies of the per-element coefficients, read by the
     // streaming sweep when the context stores coefficients in fp32 (admm_set_coeff_precision)
@@ -744,7 +749,7 @@ __device__ __forceinline__ void finalize_row(const KArgs& a, const Ctrl& cin, in
     const long long rix = (long long)i * a.q + j;
     const RowOut o = row_update(Sg, a.sb0[rix], __ldcg(a.lam + rix) * cin.f[0],
                                 __ldcg(a.p + rix) * cin.f[1], __ldcg(a.h + rix),
-                                __ldcg(a.zeta + rix), a.c[i], (double)a.n, cin.rho, dgmax, dgmin);
+                                __ldcg(a.zeta + rix), a.c[i], a.nd, cin.rho, dgmax, dgmin);
     __stcg(a.lam + rix, o.lam);
     __stcg(a.zeta + rix, o.zeta);
     __stcg(a.h + rix, o.h);
@@ -762,7 +767,7 @@ __device__ __forceinline__ void finalize_row_v(const KArgs& a, const Ctrl& cin, 
                                                double p_e, double h_o, double zeta_o, double sb0_e,
                                                double* r2, double* r3, double* s1, double* s2) {
     const long long rix = (long long)i * a.q + j;
-    const RowOut o = row_update(Sg, sb0_e, lam_e, p_e, h_o, zeta_o, a.c[i], (double)a.n, cin.rho, dgmax,
+    const RowOut o = row_update(Sg, sb0_e, lam_e, p_e, h_o, zeta_o, a.c[i], a.nd, cin.rho, dgmax,
                                 dgmin);
     __stcg(a.lam + rix, o.lam);
     __stcg(a.zeta + rix, o.zeta);
@@ -1477,7 +1482,7 @@ __global__ void __launch_bounds__(RLT ? RLT : (U == 2 ? SWEEP_LB : 256), RLT ? (
     if (tid < XB) a.xsend[tid] = acc[tid];
     if (tid == 0) {
         *a.glob_cnt = 0;
-        if (a.world == 1) {
+        if (!a.dist) {
             Ctrl& cout = a.ctrl[(it + 1) & 1];
             finalize_global(a, acc, 1, it, cin, cout, is_check);
             __threadfence();

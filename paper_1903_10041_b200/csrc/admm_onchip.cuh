@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
     const long long qn = a.q * (long long)a.n_pad;
     const long long qq = a.q;
     const DParams& P = *a.prm;
-    const double nd = (double)a.n;
+    const double nd = a.nd;
     const double qtot = (double)a.q_total;
     const bool single = (a.q_total == 1);  // q = 1: x1 = own contribution, no exchange
 

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(512) persist_kernel(KArgs a, PArgs p) {
     const int ncell = min(TC, a.n - k0);
     const long long qn = a.q * (long long)a.n_pad;
     const DParams& P = *a.prm;
-    const double nd = (double)a.n;
+    const double nd = a.nd;
 
     const long long it0 = *(volatile long long*)a.iter;
     const Ctrl& cin = a.ctrl[it0 & 1];

@@ -84,12 +84,18 @@ __device__ __forceinline__ void s2_tma(void* dst, const void* src, unsigned byte
         : "memory");
 }
 
+// first chunk (offset from the unit's start) of warp wid in the CTA's lu-th unit:
+// the assignment rotates by one warp per unit, so the short last chunk of a row
+// and the consensus cell k = 0 visit every warp in turn (balanced warps)
+__device__ __forceinline__ int s2_first(int wid, unsigned lu) { return (int)((wid - lu) & (S2_NW - 1)); }
+
 // position in one warp's chunk sequence: units u = blockIdx.x, + G, ...; chunks
-// cs + wid, + NW, ... < ce of unit u (row j); units without a chunk for this warp
-// are skipped
+// cs + s2_first, + NW, ... < ce of unit u (row j); units without a chunk for this
+// warp are skipped
 struct S2Pos {
     long long u, j;
     int c, ce;
+    unsigned lu;  // CTA-local unit count: chunk c of a unit goes to warp (c - cs + lu) mod NW
     __device__ __forceinline__ void set(const S2Args& s, int wid) {
         while (u < s.U) {
             int cs;
@@ -102,15 +108,17 @@ struct S2Pos {
                 cs = (int)(u - j * s.S) * s.TPS;
                 ce = min(s.TPR, cs + s.TPS);
             }
-            c = cs + wid;
+            c = cs + s2_first(wid, lu);
             if (c < ce) return;
             u += s.G;
+            ++lu;
         }
     }
     __device__ __forceinline__ void next(const S2Args& s, int wid) {
         c += S2_NW;
         if (c >= ce) {
             u += s.G;
+            ++lu;
             set(s, wid);
         }
     }
@@ -176,7 +184,10 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
     // row scalars (raw lam, zeta, p, h, sum b0, nu) of source i, per warp and unit parity:
     // copied with cp.async by lanes i < M one unit ahead (no registers held in flight)
     __shared__ double s_sc[S2_NW][2][6][M];
-    __shared__ double s_nue[M];            // nu after (6h), cell k = 0 (thread 0)
+    __shared__ double s_nue[S2_NW][M];     // nu after (6h), cell k = 0 (lane 0 of its warp)
+    // (6c) partials of the k = 0 cells each warp owned, in unit order: sum x_1 - nu,
+    // max, min (combined in warp order at the end: deterministic)
+    __shared__ double s_cons[S2_NW][3][M];
     __shared__ double acc[XB];
     __shared__ int s_last;
 
@@ -198,6 +209,11 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
         s_gen[tid] = 0u;
     }
     if (tid < S2_NW * M * 4) (&s_rc[0][0][0])[tid] = 0.0;
+    if (tid < S2_NW * M) {
+        s_cons[tid / M][0][tid % M] = 0.0;
+        s_cons[tid / M][1][tid % M] = -INFINITY;
+        s_cons[tid / M][2][tid % M] = INFINITY;
+    }
     if (tid < S2_NW * NS) {
         s2_bar_init(&s_full[0][0] + tid);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -207,6 +223,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
     unsigned char* const ring = s2_sm + (size_t)wid * NS * C::STAGE;  // this warp's stages
     S2Pos ahead;  // this warp's chunk NS positions ahead of the consumer: the refill of its stage
     ahead.u = blockIdx.x;
+    ahead.lu = 0;
     ahead.set(s, wid);
     for (int st = 0; st < NS && ahead.u < s.U; ++st) {
         if (lane == 0) s2_issue<M, CT>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
@@ -266,12 +283,12 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
             dgx[i] = -INFINITY;
             dgn[i] = INFINITY;
         }
-        for (int c = cs + wid; c < ce; c += S2_NW) {
+        for (int c = cs + s2_first(wid, (unsigned)unit); c < ce; c += S2_NW) {
             const int k = c * S2_TL + 2 * lane;  // first of this thread's two cells
             const unsigned char* sp = ring + (size_t)st * C::STAGE;
             s2_wait(&s_full[wid][st], ph);
             if (k < a.n_pad) {
-                const bool k0 = (k == 0);
+                const bool k0 = (k == 0) && a.k0own;
                 const bool vc0 = k < a.n, vc1 = (k + 1) < a.n;
                 double y[2], v[2], xo[M][2], xn[M][2];
                 s2_ld2<double>(sp + C::YOFF + 16 * lane, y);
@@ -292,9 +309,43 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                     double a2[2], a1[2], b2[2], b1[2];
                     s2_ld2<CT>(cp, a2);
                     s2_ld2<CT>(cp + S2_TL * sizeof(CT), a1);
+                    double Cq[2], Dq[2], bn[2], cn[2], dn[2], lo[2], hi[2];
+                    {
+                        const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
+                        const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
+                        lo[0] = tl.x; lo[1] = tl.y; hi[0] = th.x; hi[1] = th.y;
+                    }
+                    // k = 0 (consensus) cell: lazy (6h) of the previous iteration, then its
+                    // dual rescale; adds the rho4 term of (6a)
+                    auto k0_term = [&](double xoi, double& Cc, double& Dc) {
+                        double nu = sc[5][i];
+                        if (nu_pending) nu = nu + cin.x1[i] - xoi;
+                        const double nu_e = nu * cin.f[3];
+                        __stcg(a.nu + (long long)i * a.q + j, nu_e);
+                        s_nue[wid][i] = nu_e;
+                        Cc += 0.5 * R4;
+                        Dc += -R4 * (cin.x1[i] + nu_e);
+                    };
+                    if ((a.gfree >> i) & 1u) {
+                        // g = 0 on the box (b2 = b1 = 0 everywhere): the (6a) objective is the
+                        // convex quadratic (a2/q + rho3/2 [+ rho4/2]) x^2 + (a1/q - rho3 phi [...]) x;
+                        // the same C, D as below with the b terms exactly zero
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            double others = 0.0;
+#pragma unroll
+                            for (int l = 0; l < M; ++l)
+                                if (l != i) others += (l < i) ? xn[l][u] : xo[l][u];
+                            const double phi = ((s_e[u] - others) + y[u]) + mu_e[u];
+                            Cq[u] = fma(a2[u], iq, 0.5 * R3);
+                            Dq[u] = fma(a1[u], iq, -R3 * phi);
+                            if (k0 && u == 0) k0_term(xo[i][u], Cq[u], Dq[u]);
+                            xn[i][u] = clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
+                        }
+                        continue;
+                    }
                     s2_ld2<CT>(cp + 2 * S2_TL * sizeof(CT), b2);
                     s2_ld2<CT>(cp + 3 * S2_TL * sizeof(CT), b1);
-                    double Cq[2], Dq[2], bn[2], cn[2], dn[2], lo[2], hi[2];
                     bool allq = true, anyq = false;
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
@@ -307,16 +358,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                         const double e = fma(fma(b2[u], xoi, b1[u]), xoi, zl[i]);
                         Cq[u] = fma(0.5 * R1, fma(b1[u], b1[u], -2.0 * b2[u] * e), fma(a2[u], iq, 0.5 * R3));
                         Dq[u] = fma(-R1 * b1[u], e, fma(a1[u], iq, -R3 * phi));
-                        if (k0 && u == 0) {
-                            // lazy (6h) of the previous iteration, then its dual rescale
-                            double nu = sc[5][i];
-                            if (nu_pending) nu = nu + cin.x1[i] - xoi;
-                            const double nu_e = nu * cin.f[3];
-                            __stcg(a.nu + (long long)i * a.q + j, nu_e);
-                            s_nue[i] = nu_e;
-                            Cq[u] += 0.5 * R4;
-                            Dq[u] += -R4 * (cin.x1[i] + nu_e);
-                        }
+                        if (k0 && u == 0) k0_term(xoi, Cq[u], Dq[u]);
                         const bool qu = (b2[u] != 0.0);
                         allq = allq && qu;
                         anyq = anyq || qu;
@@ -324,11 +366,6 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                         bn[u] = 1.5 * (R1 * b2[u] * b1[u]) * ia2;
                         cn[u] = Cq[u] * ia2;
                         dn[u] = 0.5 * Dq[u] * ia2;
-                    }
-                    {
-                        const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
-                        const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
-                        lo[0] = tl.x; lo[1] = tl.y; hi[0] = th.x; hi[1] = th.y;
                     }
                     if (allq) {
                         double r[2];
@@ -388,13 +425,12 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                     }
                 }
                 if (k0) {
-                    // (6c) contribution x_1 - nu, in this CTA's unit order (thread 0 owns
-                    // acc[0, 3 MAXM) until the closing barrier)
+                    // (6c) contribution x_1 - nu, in this warp's unit order
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
-                        acc[i] += xn[i][0] - s_nue[i];
-                        acc[MAXM + i] = fmax(acc[MAXM + i], xn[i][0]);
-                        acc[2 * MAXM + i] = fmin(acc[2 * MAXM + i], xn[i][0]);
+                        s_cons[wid][0][i] += xn[i][0] - s_nue[wid][i];
+                        s_cons[wid][1][i] = fmax(s_cons[wid][1][i], xn[i][0]);
+                        s_cons[wid][2][i] = fmin(s_cons[wid][2][i], xn[i][0]);
                     }
                 }
             }
@@ -452,7 +488,16 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                     }
                 }
                 bool fin = true;
-                if (s.S > 1) {  // row split over segments: global exact sums, the last one finalises
+                if (a.hz) {
+                    // horizon blocks: this rank's partial row sum and dg extrema; the ranks'
+                    // values are all-reduced after the sweep and hz_rows_kernel finalises
+                    atomicAdd(a.rowacc + j * MAXM + i, part);
+                    if (chk) {
+                        atomicMax(a.hzdg + j * 2 * MAXM + i, okey(mx));
+                        atomicMax(a.hzdg + j * 2 * MAXM + MAXM + i, okey(-mn));
+                    }
+                    fin = false;
+                } else if (s.S > 1) {  // row split over segments: global exact sums, the last one finalises
                     atomicAdd(a.rowacc + j * MAXM + i, part);
                     if (chk) {
                         atomicMax(a.rowdg + j * 2 * MAXM + i, okey(mx));
@@ -476,7 +521,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                     const long long rix = (long long)i * a.q + j;
                     const RowOut o = row_update((double)(long long)part * a.fx_inv[i], sc[4][i],
                                                 sc[0][i] * cin.f[0], sc[2][i] * cin.f[1], sc[3][i], sc[1][i],
-                                                a.c[i], (double)a.n, cin.rho, mx, mn);
+                                                a.c[i], a.nd, cin.rho, mx, mn);
                     __stcg(a.lam + rix, o.lam);
                     __stcg(a.zeta + rix, o.zeta);
                     __stcg(a.h + rix, o.h);
@@ -499,7 +544,19 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
         }
     }
 
-    // ---- per-CTA partials: the check maxima (consensus partials are in acc already)
+    // ---- per-CTA partials: consensus (warps in order) and the check maxima
+    __syncthreads();
+    if (tid < M) {
+        double cs = 0.0, cx = -INFINITY, cn = INFINITY;
+        for (int w = 0; w < S2_NW; ++w) {
+            cs += s_cons[w][0][tid];
+            cx = fmax(cx, s_cons[w][1][tid]);
+            cn = fmin(cn, s_cons[w][2][tid]);
+        }
+        acc[tid] = cs;
+        acc[MAXM + tid] = cx;
+        acc[2 * MAXM + tid] = cn;
+    }
     if (chk) {
         my_r1 = warp_max(my_r1);
         my_s3 = warp_max(my_s3);
@@ -576,7 +633,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
     if (tid < XB) a.xsend[tid] = acc[tid];
     if (tid == 0) {
         *a.glob_cnt = 0;
-        if (a.world == 1) {
+        if (!a.dist) {
             Ctrl& cout = a.ctrl[(it + 1) & 1];
             finalize_global(a, acc, 1, it, cin, cout, chk);
             __threadfence();
@@ -584,6 +641,73 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
         }
     }
 }
+
+// Horizon-block sharding: after the sweep the m q fixed-point row
+// sums (rowacc) and dg extrema (hzdg) have been all-reduced over the ranks; every
+// rank finalises every row identically ((6b), (6g), (6d), (6i) via identity I1,
+// PAPER.md:432-448), adds the row check terms to the all-gathered aggregates and
+// runs the check / rho adaptation (finalize_global).  One CTA of 256 threads.
+#ifndef ADMM_KERNELS_NO_GLOBALS  // defined once, in admm.cu's translation unit
+__global__ void __launch_bounds__(256) hz_rows_kernel(KArgs a) {
+    __shared__ double red[8][4];
+    const long long it = *(volatile long long*)a.iter;
+    const Ctrl& cin = a.ctrl[it & 1];
+    if (cin.done || it >= a.prm->iter_limit) return;
+    const int ce = a.prm->check_every;
+    const bool chk = ce > 0 && ((it + 1) % ce) == 0;
+    double r2 = 0.0, r3 = 0.0, s1 = 0.0, s2 = 0.0;
+    const long long R = (long long)a.m * a.q;
+    for (long long rix = threadIdx.x; rix < R; rix += blockDim.x) {
+        const int i = (int)(rix / a.q);
+        const long long j = rix - (long long)i * a.q;
+        const unsigned long long part = a.rowacc[j * MAXM + i];
+        a.rowacc[j * MAXM + i] = 0ull;
+        double mx = okey_inv(a.hzdg[j * 2 * MAXM + i]);
+        double mn = -okey_inv(a.hzdg[j * 2 * MAXM + MAXM + i]);
+        a.hzdg[j * 2 * MAXM + i] = 0ull;
+        a.hzdg[j * 2 * MAXM + MAXM + i] = 0ull;
+        if (((a.gfree >> i) & 1u) || !chk) mx = mn = 0.0;  // dg = 0 (g-free), unused (no check)
+        const RowOut o = row_update((double)(long long)part * a.fx_inv[i], a.sb0[rix], a.lam[rix] * cin.f[0],
+                                    a.p[rix] * cin.f[1], a.h[rix], a.zeta[rix], a.c[i], a.nd, cin.rho, mx, mn);
+        a.lam[rix] = o.lam;
+        a.zeta[rix] = o.zeta;
+        a.h[rix] = o.h;
+        a.p[rix] = o.p;
+        r2 = fmax(r2, o.r2);
+        r3 = fmax(r3, o.r3);
+        s1 = fmax(s1, o.s1);
+        s2 = fmax(s2, o.s2);
+    }
+    if (chk) {
+        r2 = warp_max(r2);
+        r3 = warp_max(r3);
+        s1 = warp_max(s1);
+        s2 = warp_max(s2);
+        if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5][0] = r2;
+            red[threadIdx.x >> 5][1] = r3;
+            red[threadIdx.x >> 5][2] = s1;
+            red[threadIdx.x >> 5][3] = s2;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (chk) {
+        // the ranks reported no row terms (no row was finalised in the sweep): rank 0's
+        // slots carry the rows' terms, identical on every rank
+        double* g = a.xall;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            g[3 * MAXM + 1] = fmax(g[3 * MAXM + 1], red[w][0]);
+            g[3 * MAXM + 2] = fmax(g[3 * MAXM + 2], red[w][1]);
+            g[3 * MAXM + 3] = fmax(g[3 * MAXM + 3], red[w][2]);
+            g[3 * MAXM + 4] = fmax(g[3 * MAXM + 4], red[w][3]);
+        }
+    }
+    finalize_global(a, a.xall, a.world, it, cin, a.ctrl[(it + 1) & 1], chk);
+    __threadfence();
+    *(volatile long long*)a.iter = it + 1;
+}
+#endif
 
 // host side (sweep2.cu): kernel pointer, stage count and dynamic shared memory
 // for (m, box mode, coefficient bytes); nullptr when m is not supported

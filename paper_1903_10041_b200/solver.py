@@ -32,17 +32,23 @@ def _arr(a):
 
 
 class AdmmSolver:
-    """One ADMM context for m sources, n steps, q_total scenarios on one GPU
-    (or this rank's scenario shard when `dist` is given)."""
+    """One ADMM context for m sources, n steps, q_total scenarios on one GPU, or
+    this rank's part when `dist` (admm_dist, see dist.make_dist) is given: its
+    scenario shard [j_begin, j_end) (mode ADMM_SHARD_SCENARIOS) or its horizon
+    block [k_begin, k_end) of every scenario (ADMM_SHARD_HORIZON).  Arrays passed
+    in and returned are this rank's part ([m][q][n] with the local q and n)."""
 
     def __init__(self, m, n, q_total, device=0, dist=None, stream=None, params=None,
                  coeff_bits=64, **param_kw):
         import torch
 
-        self.m, self.n, self.q_total = int(m), int(n), int(q_total)
+        self.m, self.n_total, self.q_total = int(m), int(n), int(q_total)
         self.device = int(device)
         self.q = int(dist.j_end - dist.j_begin) if dist is not None else self.q_total
         self.j0 = int(dist.j_begin) if dist is not None else 0
+        hz = dist is not None and int(dist.mode) == _lib.ADMM_SHARD_HORIZON
+        self.k0 = int(dist.k_begin) if hz else 0
+        self.n = int(dist.k_end - dist.k_begin) if hz else self.n_total  # local horizon
         nbytes = _lib.admm_workspace_bytes(self.m, self.n, self.q, self.device)
         if nbytes == 0:
             raise AdmmError(_lib.ADMM_ERR_INVALID, "bad dimensions")
@@ -50,7 +56,7 @@ class AdmmSolver:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8,
                                      device=torch.device("cuda", self.device))
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ctx = _lib.admm_create(self.m, self.n, self.q_total, dist, self.device,
+        self.ctx = _lib.admm_create(self.m, self.n_total, self.q_total, dist, self.device,
                                     self.workspace, self.stream)
         p = params if params is not None else _lib.admm_default_params()
         for k, v in param_kw.items():

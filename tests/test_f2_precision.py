@@ -101,12 +101,14 @@ def _gpu(P, prm, iters, engine, bits=32):
 
     import paper_1903_10041_b200 as L
 
-    env = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_fx": {"ADMM_SWEEP_FX": "1"}}
-    exec_mode = {"stream": 1, "stream_fx": 1, "cluster": 2, "grid": 2}[engine]
+    env = {"grid": {"ADMM_PERSIST_GRID": "1"},
+           "stream_fx": {"ADMM_SWEEP_FX": "1", "ADMM_SWEEP2": "0"},
+           "stream_legacy": {"ADMM_SWEEP2": "0"}}
+    exec_mode = {"stream": 1, "stream_fx": 1, "stream_legacy": 1, "cluster": 2, "grid": 2}[engine]
     s = L.AdmmSolver(P["m"], P["n"], P["q"], rho=prm["rho0"], tau=prm["tau"],
                      r_bar=prm["r_bar"], sigma_bar=prm["sigma_bar"], box_mode=prm["box_mode"],
                      check_every=prm["check_every"], exec_mode=exec_mode, coeff_bits=bits)
-    for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX"):
+    for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2"):
         os.environ.pop(k, None)
     os.environ.update(env.get(engine, {}))
     try:
@@ -119,14 +121,14 @@ def _gpu(P, prm, iters, engine, bits=32):
         eng = s.engine()[0]
     finally:
         s.close()
-        for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX"):
+        for k in ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2"):
             os.environ.pop(k, None)
     return S, sol, hist, eng
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("iters", [10, 200])
-@pytest.mark.parametrize("engine", ["stream", "stream_fx", "cluster", "grid"])
+@pytest.mark.parametrize("engine", ["stream", "stream_legacy", "stream_fx", "cluster", "grid"])
 def test_gpu_fp32_coefficients_phev_q50(iters, engine):
     from test_gpu_admm import check_hist, compare_states
 
@@ -136,7 +138,7 @@ def test_gpu_fp32_coefficients_phev_q50(iters, engine):
     o = oracle.Oracle(Q, prm)
     io, ho = o.run(iters)
     Sg, sol, hg, eng = _gpu(P, prm, iters, engine)
-    assert eng == {"stream": 1, "stream_fx": 1, "cluster": 3, "grid": 2}[engine]
+    assert eng == {"stream": 4, "stream_legacy": 1, "stream_fx": 1, "cluster": 3, "grid": 2}[engine]
     compare_states(Q, o.state(), Sg)
     check_hist(ho, hg, Q, o.state())
     assert abs(sol["objective"] - io["objective"]) <= 1e-9 * abs(io["objective"])
@@ -146,7 +148,7 @@ def test_gpu_fp32_coefficients_phev_q50(iters, engine):
 @pytest.mark.parametrize("m,n,q", [(1, 5, 3), (2, 37, 3), (3, 1001, 2), (2, 2500, 2),
                                    (4, 3001, 1)])
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("engine", ["stream", "stream_fx", "cluster"])
+@pytest.mark.parametrize("engine", ["stream", "stream_legacy", "stream_fx", "cluster"])
 def test_gpu_fp32_coefficients_random(m, n, q, mode, engine):
     """Ragged tails, multi-tile rows, every m, both box modes."""
     from test_gpu_admm import check_hist, compare_states
@@ -195,7 +197,7 @@ def test_gpu_fp32_sweep_full_size_sampled():
     eng = s.engine()[0]
     s.close()
     del P
-    assert eng == 1
+    assert eng == 4  # the TMA sweep reads the fp32 coefficient copies
     xs = x.reshape(2, reps, 50, 1000)
     assert np.array_equal(xs.min(axis=1), xs.max(axis=1)), "copies diverged"
     o = _replicated_oracle(round32(base), reps, prm)
