@@ -52,10 +52,20 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     if verbose:
         common.insert(1, "-Xptxas=-v")
     units = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "admm.h"), __file__]
+    hdr_t = max(os.path.getmtime(h) for h in headers)
     procs, objs = [], []
     for u in units:
         o = os.path.join(odir, os.path.basename(u)[:-3] + ".o")
         objs.append(o)
+        # an object is reused when it is newer than its unit and every header (any unit
+        # may include any header) and was built with the same flags
+        flags_file = o + ".flags"
+        same_flags = os.path.exists(flags_file) and open(flags_file).read() == " ".join(common)
+        if (not force and same_flags and os.path.exists(o)
+                and os.path.getmtime(o) >= max(hdr_t, os.path.getmtime(u))):
+            continue
+        open(flags_file, "w").write(" ".join(common))
         procs.append((u, subprocess.Popen(common + ["-c", "-o", o, u], stdout=subprocess.PIPE,
                                           stderr=subprocess.PIPE, text=True)))
     failed = False

@@ -662,16 +662,16 @@ admm_status plan_stream(admm_ctx* ctx) {
     const char* opt = getenv("ADMM_SWEEP2");
     if (opt && opt[0] == '0') return ADMM_OK;
     if (!ctx->fx_ok || ctx->m > 4) return ADMM_OK;
-    int ns = 0;
+    int ns = 0, tl = 0;
     size_t smem = 0;
-    const void* fn = sweep2_pick(ctx->m, ctx->params.box_mode, ctx->coeff_bits / 8, &ns, &smem);
+    const void* fn = sweep2_pick(ctx->m, ctx->params.box_mode, ctx->coeff_bits / 8, ctx->q, &ns, &smem, &tl);
     if (!fn) return ADMM_OK;
     CKC(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, S2_NT, smem));
     if (occ < 1) return ADMM_OK;
     occ = std::min(occ, 32);
-    ctx->s2 = sweep2_plan(ctx->q, ctx->n_pad, occ * ctx->sms);
+    ctx->s2 = sweep2_plan(ctx->q, ctx->n_pad, tl, occ * ctx->sms);
     ctx->s2_fn = fn;
     ctx->s2_smem = smem;
     ctx->use_tma = true;
@@ -679,8 +679,8 @@ admm_status plan_stream(admm_ctx* ctx) {
         if (dbg[0] == '1') {
             cudaFuncAttributes fa;
             if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess)
-                fprintf(stderr, "[admm] sweep2: regs %d local %zu smem %zu+%zu occ %d G %d S %d TPS %d TPR %d\n",
-                        fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes, smem, occ, ctx->s2.G, ctx->s2.S,
+                fprintf(stderr, "[admm] sweep2: chunk %d regs %d local %zu smem %zu+%zu occ %d G %d S %d TPS %d TPR %d\n",
+                        tl, fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes, smem, occ, ctx->s2.G, ctx->s2.S,
                         ctx->s2.TPS, ctx->s2.TPR);
         }
     }
@@ -900,6 +900,11 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
     std::vector<long long> cand;
     for (long long T = T0; T >= 1; --T) cand.push_back(T);
     for (long long T = T0 + 1; T <= ONCHIP_MAX_T; ++T) cand.push_back(T);
+    // experiments: ADMM_CLUSTER_T forces the tiles per row, ADMM_CLUSTER_WARPS caps the
+    // bulk warps per CTA (more cells per thread, smaller CTAs, more CTAs per SM)
+    if (const char* e = getenv("ADMM_CLUSTER_T")) cand.assign(1, std::max(1LL, atoll(e)));
+    int wcap = ONCHIP_MAX_WARPS - 1;
+    if (const char* e = getenv("ADMM_CLUSTER_WARPS")) wcap = std::max(1, std::min(wcap, atoi(e)));
     for (long long T : cand) {
         long long TC0 = n, TC = n;
         if (T > 1) {
@@ -912,7 +917,7 @@ PPlan plan_cluster(admm_ctx* ctx, cluster_fn fn) {
         if (smem > 200 * 1024 || TCM > 4 * 512) continue;
         const long long G = q * T;
         if (G > 32LL * sms) continue;
-        const int nbw = (int)std::min<long long>(ONCHIP_MAX_WARPS - 1, (TCM + 31) / 32);
+        const int nbw = (int)std::min<long long>(wcap, (TCM + 31) / 32);
         const int BS = (nbw + 1) * 32;
         if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess) {

@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                         for (int i = 0; i < M; ++i) {
                             const double b2 = s_b2[i * TCM + c], b1 = s_b1[i * TCM + c];
                             s_x[i * TCM + c] = txn[i];
+                            if ((a.gfree >> i) & 1u) continue;  // g = 0: no row sum, dg = 0
                             fx[i] += __double2ll_rn(fma(b2, txn[i], b1) * txn[i] * fxs[i]);
                             if (is_check) {
                                 const double dg = (txn[i] - txo[i]) * fma(b2, txn[i] + txo[i], b1);
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
                         s_x[i * TCM + c] = xn[i];
+                        if ((a.gfree >> i) & 1u) continue;
                         fx[i] += __double2ll_rn(fma(cb2[i], xn[i], cb1[i]) * xn[i] * fxs[i]);
                         if (is_check) {
                             const double dg = (xn[i] - xo[i]) * fma(cb2[i], xn[i] + xo[i], cb1[i]);
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(ONCHIP_MAX_WARPS * 32) persist_cluster_kernel(
                     mx = fmax(mx, s_dgp[t][tid]);
                     mn = fmin(mn, s_dgp[t][M + tid]);
                 }
+            if ((a.gfree >> tid) & 1u) mx = mn = 0.0;  // g-free source: dg = 0 for every k
             const double W = (sg + r_sb0) - nd * r_lam;
             const double t = (r_h + r_p) - W;
             const double lam = s_kap * t;

@@ -31,7 +31,7 @@
 namespace admm_dev {
 
 struct S2Args {
-    int TPR;      // chunks per row (ceil(n_pad / 64))
+    int TPR;      // chunks per row (ceil(n_pad / chunk))
     int S;        // segments per row
     int TPS;      // chunks per segment
     int G;        // grid size
@@ -40,16 +40,20 @@ struct S2Args {
 
 constexpr int S2_NT = 128;  // threads per CTA
 constexpr int S2_NW = S2_NT / 32;
-constexpr int S2_TL = 64;   // cells per chunk (two per lane of one warp)
 constexpr int S2_UB = 4;    // unit slots of the row partials (flow-controlled by s_gen)
 
-// one stage of a warp's ring: x_i (M, fp64), y, v (fp64), then a2_i, a1_i, b2_i, b1_i (CT)
-template <int M, typename CT>
+// one stage of a warp's ring (chunk of TL = 32 L cells, L cells per lane): x_i (M, fp64),
+// y, v (fp64), a2_i, a1_i, b2_i, b1_i (CT), and with BX the box lo_i, hi_i (fp64: horizon-
+// type problems, where the box is not shared by many rows and would be an HBM stream of
+// its own read through L1)
+template <int M, typename CT, int L, bool BX>
 struct S2Cfg {
-    static constexpr int YOFF = M * S2_TL * 8;
-    static constexpr int VOFF = (M + 1) * S2_TL * 8;
-    static constexpr int COFF = (M + 2) * S2_TL * 8;
-    static constexpr int STAGE = COFF + 4 * M * S2_TL * (int)sizeof(CT);
+    static constexpr int TL = 32 * L;
+    static constexpr int YOFF = M * TL * 8;
+    static constexpr int VOFF = (M + 1) * TL * 8;
+    static constexpr int COFF = (M + 2) * TL * 8;
+    static constexpr int BOFF = COFF + 4 * M * TL * (int)sizeof(CT);
+    static constexpr int STAGE = BOFF + (BX ? 2 * M * TL * 8 : 0);
 };
 
 __device__ __forceinline__ unsigned s2_smem(const void* p) {
@@ -124,18 +128,26 @@ struct S2Pos {
     }
 };
 
-template <int M, typename CT>
+template <int M, typename CT, int L, bool BX>
 __device__ __forceinline__ void s2_issue(const KArgs& a, long long j, int t, unsigned char* st,
                                          unsigned long long* bar) {
-    using C = S2Cfg<M, CT>;
-    const int k0 = t * S2_TL;
-    const int nc = min(S2_TL, a.n_pad - k0);  // n_pad % 4 == 0: byte counts are multiples of 16
+    using C = S2Cfg<M, CT, L, BX>;
+    constexpr int TL = C::TL;
+    const int k0 = t * TL;
+    const int nc = min(TL, a.n_pad - k0);  // n_pad % 4 == 0: byte counts are multiples of 16
     const unsigned b8 = (unsigned)nc * 8u, bc = (unsigned)nc * (unsigned)sizeof(CT);
-    s2_expect(bar, (unsigned)(M + 2) * b8 + 4u * M * bc);
+    s2_expect(bar, (unsigned)(M + 2 + (BX ? 2 * M : 0)) * b8 + 4u * M * bc);
     const long long qn = a.q * (long long)a.n_pad;
     const long long row = j * a.n_pad + k0;
 #pragma unroll
-    for (int i = 0; i < M; ++i) s2_tma(st + (size_t)i * S2_TL * 8, a.x + i * qn + row, b8, bar);
+    for (int i = 0; i < M; ++i) s2_tma(st + (size_t)i * TL * 8, a.x + i * qn + row, b8, bar);
+    if constexpr (BX) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            s2_tma(st + C::BOFF + (size_t)(2 * i) * TL * 8, a.lo + (long long)i * a.n_pad + k0, b8, bar);
+            s2_tma(st + C::BOFF + (size_t)(2 * i + 1) * TL * 8, a.hi + (long long)i * a.n_pad + k0, b8, bar);
+        }
+    }
     s2_tma(st + C::YOFF, a.y + row, b8, bar);
     s2_tma(st + C::VOFF, a.v + row, b8, bar);
     const CT* src[4];
@@ -149,13 +161,15 @@ __device__ __forceinline__ void s2_issue(const KArgs& a, long long j, int t, uns
     for (int i = 0; i < M; ++i)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-            s2_tma(st + C::COFF + (size_t)(4 * i + c) * S2_TL * sizeof(CT), src[c] + i * qn + row, bc, bar);
+            s2_tma(st + C::COFF + (size_t)(4 * i + c) * TL * sizeof(CT), src[c] + i * qn + row, bc, bar);
 }
 
-// two consecutive values of a shared-memory stream (fp64 or fp32), widened
-template <typename CT>
-__device__ __forceinline__ void s2_ld2(const unsigned char* p, double* o) {
-    if constexpr (sizeof(CT) == 8) {
+// L consecutive values of a shared-memory stream (fp64 or fp32), widened
+template <typename CT, int L>
+__device__ __forceinline__ void s2_ldL(const unsigned char* p, double* o) {
+    if constexpr (L == 1) {
+        o[0] = (double)*reinterpret_cast<const CT*>(p);
+    } else if constexpr (sizeof(CT) == 8) {
         const double2 t = *reinterpret_cast<const double2*>(p);
         o[0] = t.x;
         o[1] = t.y;
@@ -165,14 +179,23 @@ __device__ __forceinline__ void s2_ld2(const unsigned char* p, double* o) {
         o[1] = (double)t.y;
     }
 }
+template <int L>
+__device__ __forceinline__ void s2_stL(double* p, const double* v) {
+    if constexpr (L == 1) *p = v[0];
+    else *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+}
 
 #ifndef SWEEP2_MINB
 #define SWEEP2_MINB 4
 #endif
 
-template <int M, int MODE, typename CT, int NS>
-__global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel(KArgs a, S2Args s) {
-    using C = S2Cfg<M, CT>;
+// L = 2: two cells per lane (M <= 2, many rows: the configs[3] kernel); L = 1 with the box
+// staged (BX): horizon-type problems (few rows, M up to 4) -- half the registers per lane,
+// so more warps per SM, and no L1 misses on the box
+template <int M, int MODE, typename CT, int NS, int L, bool BX>
+__global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)) sweep2_kernel(KArgs a, S2Args s) {
+    using C = S2Cfg<M, CT, L, BX>;
+    constexpr int TL = C::TL;
     extern __shared__ __align__(128) unsigned char s2_sm[];
     __shared__ __align__(8) unsigned long long s_full[S2_NW][NS];  // per-warp rings
     __shared__ unsigned long long s_fxw[S2_UB][S2_NW][M];  // per-warp fixed-point row partials
@@ -226,7 +249,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
     ahead.lu = 0;
     ahead.set(s, wid);
     for (int st = 0; st < NS && ahead.u < s.U; ++st) {
-        if (lane == 0) s2_issue<M, CT>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+        if (lane == 0) s2_issue<M, CT, L, BX>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
         ahead.next(s, wid);
     }
 
@@ -284,36 +307,44 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
             dgn[i] = INFINITY;
         }
         for (int c = cs + s2_first(wid, (unsigned)unit); c < ce; c += S2_NW) {
-            const int k = c * S2_TL + 2 * lane;  // first of this thread's two cells
+            const int k = c * TL + L * lane;  // first of this thread's L cells
             const unsigned char* sp = ring + (size_t)st * C::STAGE;
             s2_wait(&s_full[wid][st], ph);
             if (k < a.n_pad) {
                 const bool k0 = (k == 0) && a.k0own;
-                const bool vc0 = k < a.n, vc1 = (k + 1) < a.n;
-                double y[2], v[2], xo[M][2], xn[M][2];
-                s2_ld2<double>(sp + C::YOFF + 16 * lane, y);
-                s2_ld2<double>(sp + C::VOFF + 16 * lane, v);
+                bool vc[L];
 #pragma unroll
-                for (int i = 0; i < M; ++i) s2_ld2<double>(sp + (size_t)i * S2_TL * 8 + 16 * lane, xo[i]);
-                double s_e[2], mu_e[2];
+                for (int u = 0; u < L; ++u) vc[u] = (k + u) < a.n;
+                double y[L], v[L], xo[M][L], xn[M][L];
+                s2_ldL<double, L>(sp + C::YOFF + 8 * L * lane, y);
+                s2_ldL<double, L>(sp + C::VOFF + 8 * L * lane, v);
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int i = 0; i < M; ++i) s2_ldL<double, L>(sp + (size_t)i * TL * 8 + 8 * L * lane, xo[i]);
+                double s_e[L], mu_e[L];
+#pragma unroll
+                for (int u = 0; u < L; ++u) {
                     s_e[u] = fmax(v[u], 0.0);
                     mu_e[u] = v[u] < 0.0 ? -v[u] * f2 : 0.0;
                 }
                 // ---- (6a) Gauss-Seidel over sources (same arithmetic as gs_cellU)
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i) * S2_TL * sizeof(CT) +
-                                              2 * sizeof(CT) * lane;
-                    double a2[2], a1[2], b2[2], b1[2];
-                    s2_ld2<CT>(cp, a2);
-                    s2_ld2<CT>(cp + S2_TL * sizeof(CT), a1);
-                    double Cq[2], Dq[2], bn[2], cn[2], dn[2], lo[2], hi[2];
-                    {
+                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i) * TL * sizeof(CT) +
+                                              L * sizeof(CT) * lane;
+                    double a2[L], a1[L], b2[L], b1[L];
+                    s2_ldL<CT, L>(cp, a2);
+                    s2_ldL<CT, L>(cp + TL * sizeof(CT), a1);
+                    double Cq[L], Dq[L], bn[L], cn[L], dn[L], lo[L], hi[L];
+                    if constexpr (BX) {
+                        s2_ldL<double, L>(sp + C::BOFF + (size_t)(2 * i) * TL * 8 + 8 * L * lane, lo);
+                        s2_ldL<double, L>(sp + C::BOFF + (size_t)(2 * i + 1) * TL * 8 + 8 * L * lane, hi);
+                    } else if constexpr (L == 2) {
                         const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
                         const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
                         lo[0] = tl.x; lo[1] = tl.y; hi[0] = th.x; hi[1] = th.y;
+                    } else {
+                        lo[0] = __ldg(a.lo + (long long)i * a.n_pad + k);
+                        hi[0] = __ldg(a.hi + (long long)i * a.n_pad + k);
                     }
                     // k = 0 (consensus) cell: lazy (6h) of the previous iteration, then its
                     // dual rescale; adds the rho4 term of (6a)
@@ -331,7 +362,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                         // convex quadratic (a2/q + rho3/2 [+ rho4/2]) x^2 + (a1/q - rho3 phi [...]) x;
                         // the same C, D as below with the b terms exactly zero
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
+                        for (int u = 0; u < L; ++u) {
                             double others = 0.0;
 #pragma unroll
                             for (int l = 0; l < M; ++l)
@@ -344,11 +375,11 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                         }
                         continue;
                     }
-                    s2_ld2<CT>(cp + 2 * S2_TL * sizeof(CT), b2);
-                    s2_ld2<CT>(cp + 3 * S2_TL * sizeof(CT), b1);
+                    s2_ldL<CT, L>(cp + 2 * TL * sizeof(CT), b2);
+                    s2_ldL<CT, L>(cp + 3 * TL * sizeof(CT), b1);
                     bool allq = true, anyq = false;
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
+                    for (int u = 0; u < L; ++u) {
                         double others = 0.0;
 #pragma unroll
                         for (int l = 0; l < M; ++l)
@@ -368,53 +399,54 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
                         dn[u] = 0.5 * Dq[u] * ia2;
                     }
                     if (allq) {
-                        double r[2];
-                        quartic_coreU<MODE, 2>(bn, cn, dn, Cq, Dq, lo, hi, r);
-                        xn[i][0] = r[0];
-                        xn[i][1] = r[1];
+                        double r[L];
+                        quartic_coreU<MODE, L>(bn, cn, dn, Cq, Dq, lo, hi, r);
+#pragma unroll
+                        for (int u = 0; u < L; ++u) xn[i][u] = r[u];
                     } else if (!anyq) {  // a source without g (A = B = 0): quadratic
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) xn[i][u] = clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
+                        for (int u = 0; u < L; ++u) xn[i][u] = clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
                     } else {
 #pragma unroll
-                        for (int u = 0; u < 2; ++u)
+                        for (int u = 0; u < L; ++u)
                             xn[i][u] = (b2[u] != 0.0) ? quartic_core<MODE>(bn[u], cn[u], dn[u], Cq[u], Dq[u], lo[u], hi[u])
                                                       : clampd(-Dq[u] * rcp_nr(2.0 * Cq[u]), lo[u], hi[u]);
                     }
                 }
                 // ---- (6e)/(6f) per cell, reduced state v = s - mu (identity I2)
-                double vn[2];
+                double vn[L];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < L; ++u) {
                     double txo[M], txn[M];
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
                         txo[i] = xo[i][u];
                         txn[i] = xn[i][u];
                     }
-                    const bool valid = u == 0 ? vc0 : vc1;
+                    const bool valid = vc[u];
                     double r1l = my_r1, s3l = my_s3;
                     const double vnew = cell_tail<M>(txo, txn, y[u], v[u], f2, chk && valid, r1l, s3l);
                     my_r1 = r1l;
                     my_s3 = s3l;
                     vn[u] = valid ? vnew : 0.0;
                 }
-                *reinterpret_cast<double2*>(a.v + j * a.n_pad + k) = make_double2(vn[0], vn[1]);
+                s2_stL<L>(a.v + j * a.n_pad + k, vn);
                 // ---- row partials: exact fixed point, dg extrema on checks
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i + 2) * S2_TL * sizeof(CT) +
-                                              2 * sizeof(CT) * lane;
-                    double b2[2], b1[2];
-                    s2_ld2<CT>(cp, b2);
-                    s2_ld2<CT>(cp + S2_TL * sizeof(CT), b1);
-                    if (!vc0) xn[i][0] = 0.0;  // padding stays 0
-                    if (!vc1) xn[i][1] = 0.0;
-                    *reinterpret_cast<double2*>(a.x + i * qn + j * a.n_pad + k) = make_double2(xn[i][0], xn[i][1]);
+                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i + 2) * TL * sizeof(CT) +
+                                              L * sizeof(CT) * lane;
+                    double b2[L], b1[L];
+                    s2_ldL<CT, L>(cp, b2);
+                    s2_ldL<CT, L>(cp + TL * sizeof(CT), b1);
+#pragma unroll
+                    for (int u = 0; u < L; ++u)
+                        if (!vc[u]) xn[i][u] = 0.0;  // padding stays 0
+                    s2_stL<L>(a.x + i * qn + j * a.n_pad + k, xn[i]);
                     if ((a.gfree >> i) & 1u) continue;  // g = 0 on the box: no row sum, dg = 0
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (u == 0 ? vc0 : vc1) {
+                    for (int u = 0; u < L; ++u) {
+                        if (vc[u]) {
                             fx[i] += __double2ll_rn(fma(b2[u], xn[i][u], b1[u]) * xn[i][u] * a.fx_scale[i]);
                             if (chk) {  // sigma's z-term only
                                 const double dg = (xn[i][u] - xo[i][u]) * fma(b2[u], xn[i][u] + xo[i][u], b1[u]);
@@ -438,7 +470,7 @@ __global__ void __launch_bounds__(S2_NT, M <= 2 ? SWEEP2_MINB : 2) sweep2_kernel
             if (lane == 0 && ahead.u < s.U) {
                 // refill the stage with this warp's chunk NS positions ahead
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                s2_issue<M, CT>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+                s2_issue<M, CT, L, BX>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
             }
             ahead.next(s, wid);
             if (++st == NS) {
@@ -711,8 +743,9 @@ __global__ void __launch_bounds__(256) hz_rows_kernel(KArgs a) {
 
 // host side (sweep2.cu): kernel pointer, stage count and dynamic shared memory
 // for (m, box mode, coefficient bytes); nullptr when m is not supported
-const void* sweep2_pick(int m, int mode, int coeff_bytes, int* ns, size_t* smem);
-// work decomposition for q rows of n_pad cells over at most g_max CTAs
-S2Args sweep2_plan(long long q, long long n_pad, int g_max);
+// and the chunk length it streams (64 cells: two per lane, or 32 with the box staged)
+const void* sweep2_pick(int m, int mode, int coeff_bytes, long long q, int* ns, size_t* smem, int* tl);
+// work decomposition for q rows of n_pad cells in chunks of tl over at most g_max CTAs
+S2Args sweep2_plan(long long q, long long n_pad, int tl, int g_max);
 
 }  // namespace admm_dev

@@ -11,24 +11,34 @@
 
 namespace admm_dev {
 
-// stages of each warp's ring: two (6 KB each at m = 2: four CTAs per SM, 192 KB);
-// ADMM_S2_NS=3 for experiments
-const void* sweep2_pick(int m, int mode, int coeff_bytes, int* ns, size_t* smem) {
-    int want = 2;
-    if (const char* e = getenv("ADMM_S2_NS")) want = atoi(e) == 3 ? 3 : 2;
-#define S2K(MM, CT, NN)                                                                           \
-    if (m == MM && want == NN) {                                                                  \
-        *ns = NN;                                                                                 \
-        *smem = (size_t)S2_NW * NN * S2Cfg<MM, CT>::STAGE;                                                \
-        return mode == BOX_EXACT ? (const void*)sweep2_kernel<MM, BOX_EXACT, CT, NN>              \
-                                 : (const void*)sweep2_kernel<MM, BOX_PROJECT, CT, NN>;          \
+// Kernel choice.  Many rows (q >= 16, the box shared by every row and L1/L2-resident):
+// two cells per lane, 64-cell chunks (four CTAs per SM at m <= 2).  Few rows (horizon-type
+// problems): one cell per lane with the box staged by TMA next to the coefficients
+// (32-cell chunks, up to three CTAs per SM at m = 4).  ADMM_S2_L=1/2 forces the layout.
+// Two ring stages per warp.
+const void* sweep2_pick(int m, int mode, int coeff_bytes, long long q, int* ns, size_t* smem, int* tl) {
+    bool one = q < 16;
+    if (const char* e = getenv("ADMM_S2_L")) one = (e[0] == '1');
+#define S2K(MM, CT, LL, BB)                                                                      \
+    if (m == MM) {                                                                               \
+        *ns = 2;                                                                                 \
+        *tl = S2Cfg<MM, CT, LL, BB>::TL;                                                         \
+        *smem = (size_t)S2_NW * 2 * S2Cfg<MM, CT, LL, BB>::STAGE;                                \
+        return mode == BOX_EXACT ? (const void*)sweep2_kernel<MM, BOX_EXACT, CT, 2, LL, BB>      \
+                                 : (const void*)sweep2_kernel<MM, BOX_PROJECT, CT, 2, LL, BB>;  \
     }
     if (coeff_bytes == 8) {
-        S2K(1, double, 2) S2K(2, double, 2) S2K(3, double, 2) S2K(4, double, 2)
-        S2K(1, double, 3) S2K(2, double, 3) S2K(3, double, 3) S2K(4, double, 3)
+        if (one) {
+            S2K(1, double, 1, true) S2K(2, double, 1, true) S2K(3, double, 1, true) S2K(4, double, 1, true)
+        } else {
+            S2K(1, double, 2, false) S2K(2, double, 2, false) S2K(3, double, 2, false) S2K(4, double, 2, false)
+        }
     } else {
-        S2K(1, float, 2) S2K(2, float, 2) S2K(3, float, 2) S2K(4, float, 2)
-        S2K(1, float, 3) S2K(2, float, 3) S2K(3, float, 3) S2K(4, float, 3)
+        if (one) {
+            S2K(1, float, 1, true) S2K(2, float, 1, true) S2K(3, float, 1, true) S2K(4, float, 1, true)
+        } else {
+            S2K(1, float, 2, false) S2K(2, float, 2, false) S2K(3, float, 2, false) S2K(4, float, 2, false)
+        }
     }
 #undef S2K
     return nullptr;
@@ -37,9 +47,9 @@ const void* sweep2_pick(int m, int mode, int coeff_bytes, int* ns, size_t* smem)
 // Units = (row, segment of TPS tiles).  Whole rows (S = 1) unless splitting rows
 // balances the CTAs better: the estimated time of a split is the largest unit count
 // of a CTA x its tiles per unit (+2 % per extra segment for the global row atomics).
-S2Args sweep2_plan(long long q, long long n_pad, int g_max) {
+S2Args sweep2_plan(long long q, long long n_pad, int tl, int g_max) {
     S2Args s{};
-    s.TPR = (int)((n_pad + S2_TL - 1) / S2_TL);
+    s.TPR = (int)((n_pad + tl - 1) / tl);
     double best = 1e300;
     int best_S = 1;
     for (int S = 1; S <= s.TPR; ++S) {
@@ -54,6 +64,7 @@ S2Args sweep2_plan(long long q, long long n_pad, int g_max) {
         }
         if (U >= 64LL * g_max) break;
     }
+    if (const char* e = getenv("ADMM_S2_S")) best_S = std::max(1, std::min(s.TPR, atoi(e)));  // experiments
     s.TPS = (s.TPR + best_S - 1) / best_S;
     s.S = (s.TPR + s.TPS - 1) / s.TPS;
     s.U = q * s.S;

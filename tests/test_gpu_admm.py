@@ -48,24 +48,26 @@ def compare_states(P, So, Sg, tol=1e-9):
 
 # streaming engine (the TMA sweep sweep2_kernel for finite boxes) + graph while loop;
 # persistent with rows in clusters; persistent with a grid barrier per iteration
-# (forced through ADMM_PERSIST_GRID=1).  ALT_ENGINES: the TMA sweep with a 3-stage
-# ring (ADMM_S2_NS=3) and the register-fed sweep_kernel (ADMM_SWEEP2=0) with its
+# (forced through ADMM_PERSIST_GRID=1).  ALT_ENGINES: the TMA sweep with its other
+# layout forced (ADMM_S2_L=1: one cell per lane + staged box, the few-rows layout;
+# ADMM_S2_L=2: two cells per lane, the many-rows layout) and the register-fed
+# sweep_kernel (ADMM_SWEEP2=0) with its
 # measured-but-not-default variants: the barrier-free fixed-point epilogue on every
 # shape (ADMM_SWEEP_FX=1), four cells per thread staged through shared memory
 # (ADMM_SWEEP_CPT=4), cp.async prefetch of the next item with fixed-point slots
 # (ADMM_SWEEP_PF=1) or block barriers (=2), the row loop with 128-thread CTAs
 # (ADMM_SWEEP_RL=1).  Read at solver creation.
 ENGINES = ["stream", "cluster", "grid"]
-ALT_ENGINES = ["stream_ns3", "stream_legacy", "stream_fx", "stream_u4", "stream_pf", "stream_pf2",
-               "stream_rl"]
-_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_ns3": 1, "stream_legacy": 1, "stream_fx": 1,
+ALT_ENGINES = ["stream_l1", "stream_l2", "stream_legacy", "stream_fx", "stream_u4", "stream_pf",
+               "stream_pf2", "stream_rl"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_l1": 1, "stream_l2": 1, "stream_legacy": 1, "stream_fx": 1,
          "stream_pf": 1, "stream_pf2": 1, "stream_u4": 1, "stream_rl": 1, 0: 0}
 _LEG = {"ADMM_SWEEP2": "0"}
-_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_ns3": {"ADMM_S2_NS": "3"},
+_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_l1": {"ADMM_S2_L": "1"}, "stream_l2": {"ADMM_S2_L": "2"},
         "stream_legacy": _LEG, "stream_fx": {"ADMM_SWEEP_FX": "1", **_LEG},
         "stream_pf": {"ADMM_SWEEP_PF": "1", **_LEG}, "stream_pf2": {"ADMM_SWEEP_PF": "2", **_LEG},
         "stream_u4": {"ADMM_SWEEP_CPT": "4", **_LEG}, "stream_rl": {"ADMM_SWEEP_RL": "1", **_LEG}}
-_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2", "ADMM_S2_NS", "ADMM_SWEEP_PF",
+_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2", "ADMM_S2_L", "ADMM_SWEEP_PF",
              "ADMM_SWEEP_CPT", "ADMM_SWEEP_RL")
 
 
