@@ -13,6 +13,7 @@
 //     ncclAllGather -> hz_rows_kernel] (horizon blocks), driven by a host loop
 //     that polls the done flag once per body.
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -71,10 +72,12 @@ Layout make_layout(int m, long long n, long long q, int sms) {
         o = align_up(o + std::max<size_t>(bytes, 8), 256);
         return r;
     };
-    L.a2 = take(E); L.a1 = take(E); L.a0 = take(E); L.b2 = take(E); L.b1 = take(E); L.b0 = take(E);
+    // a2, a1, b2, b1 at one stride (the TMA sweep fetches the four with one 4-D tensor
+    // copy), lo/hi and y/v adjacent likewise
+    L.a2 = take(E); L.a1 = take(E); L.b2 = take(E); L.b1 = take(E); L.a0 = take(E); L.b0 = take(E);
     L.lo = take((size_t)m * n_pad * 8); L.hi = take((size_t)m * n_pad * 8);
-    L.y = take(Cc); L.c = take((size_t)m * 8); L.sb0 = take(R);
-    L.x = take(E); L.v = take(Cc);
+    L.y = take(Cc); L.v = take(Cc); L.c = take((size_t)m * 8); L.sb0 = take(R);
+    L.x = take(E);
     L.lam = take(R); L.zeta = take(R); L.h = take(R); L.p = take(R); L.nu = take(R);
     L.cta_part = take((size_t)32 * sms * XB * 8);
     L.row_part = take(T > 1 ? (size_t)m * q * T * 3 * 8 : 8);
@@ -507,6 +510,7 @@ struct admm_ctx {
     double fx_scale[MAXM] = {}, fx_inv[MAXM] = {};
     bool use_tma = false;         // streaming engine: the TMA sweep (sweep2_kernel) runs
     const void* s2_fn = nullptr;  // sweep2_kernel instantiation of the current plan
+    S2Maps s2maps{};              // its TMA tensor maps
     size_t s2_smem = 0;           // its dynamic shared memory (the stage ring)
     int coeff_bits = 64;          // F2: storage precision of a2, a1, b2, b1 (64 or 32)
     int cpt = 2;                  // streaming sweep: cells per thread (2, or 4 for m <= 2)
@@ -654,6 +658,66 @@ sweep_fn pick_sweep(int m, int mode, bool fx, bool f32, bool pf, int cpt, int rl
 bool use_pf_sweep(const admm_ctx* ctx);
 size_t pf_smem_bytes(const admm_ctx* ctx);
 
+// TMA tensor maps (driver entry point cuTensorMapEncodeTiled, no libcuda link needed)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+bool tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+          const cuuint64_t* strides, const cuuint32_t* box) {
+    auto fn = tmap_encoder();
+    if (!fn) return false;
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the four maps of the TMA sweep for chunks of tl cells (admm_sweep2.cuh S2Maps)
+bool build_s2_maps(admm_ctx* ctx, int tl) {
+    const KArgs& a = ctx->ka;
+    const Layout& L = ctx->L;
+    const cuuint64_t np = (cuuint64_t)ctx->n_pad, q = (cuuint64_t)ctx->q, m = (cuuint64_t)ctx->m;
+    const cuuint32_t T = (cuuint32_t)tl, M = (cuuint32_t)ctx->m;
+    S2Maps& t = ctx->s2maps;
+    {
+        const cuuint64_t dims[3] = {np, q, m}, str[2] = {np * 8, q * np * 8};
+        const cuuint32_t box[3] = {T, 1, M};
+        if (!tmap(&t.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.x, dims, str, box)) return false;
+    }
+    {
+        const bool f32 = ctx->coeff_bits == 32;
+        const cuuint64_t es = f32 ? 4 : 8;
+        const cuuint64_t cstr = f32 ? m * q * np * 4 : (cuuint64_t)(L.a1 - L.a2);
+        if (!f32 && ((cuuint64_t)(L.b2 - L.a1) != cstr || (cuuint64_t)(L.b1 - L.b2) != cstr)) return false;
+        const cuuint64_t dims[4] = {np, q, m, 4}, str[3] = {np * es, q * np * es, cstr};
+        const cuuint32_t box[4] = {T, 1, M, 4};
+        const void* base = f32 ? (const void*)a.fa2 : (const void*)a.a2;
+        if (!tmap(&t.c, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims,
+                  str, box))
+            return false;
+    }
+    {
+        const cuuint64_t dims[3] = {np, q, 2}, str[2] = {np * 8, (cuuint64_t)(L.v - L.y)};
+        const cuuint32_t box[3] = {T, 1, 2};
+        if (!tmap(&t.yv, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.y, dims, str, box)) return false;
+    }
+    {
+        const cuuint64_t dims[3] = {np, m, 2}, str[2] = {np * 8, (cuuint64_t)(L.hi - L.lo)};
+        const cuuint32_t box[3] = {T, M, 2};
+        if (!tmap(&t.box, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.lo, dims, str, box)) return false;
+    }
+    return true;
+}
+
 // streaming engine: the TMA sweep (admm_sweep2.cuh) whenever the fixed-point row
 // scales exist (finite boxes) and m <= 4; ADMM_SWEEP2=0 selects the register-fed
 // sweep_kernel (kept for infinite bounds and as a measured alternative)
@@ -671,6 +735,7 @@ admm_status plan_stream(admm_ctx* ctx) {
     CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, S2_NT, smem));
     if (occ < 1) return ADMM_OK;
     occ = std::min(occ, 32);
+    if (!build_s2_maps(ctx, tl)) return ADMM_OK;  // no tensor maps: the register-fed sweep
     ctx->s2 = sweep2_plan(ctx->q, ctx->n_pad, tl, occ * ctx->sms);
     ctx->s2_fn = fn;
     ctx->s2_smem = smem;
@@ -692,7 +757,7 @@ admm_status record_body(admm_ctx* ctx, sweep_fn fn, cudaStream_t st) {
     const int K = std::max(1, ctx->params.check_every);
     for (int r = 0; r < K; ++r) {
         if (ctx->use_tma) {
-            void* args[] = {(void*)&ctx->ka, (void*)&ctx->s2};
+            void* args[] = {(void*)&ctx->ka, (void*)&ctx->s2, (void*)&ctx->s2maps};
             CKC(cudaLaunchKernel(ctx->s2_fn, dim3((unsigned)ctx->s2.G), dim3(S2_NT), args, ctx->s2_smem, st));
         } else
             fn<<<ctx->G, ctx->bs, pf_smem_bytes(ctx), st>>>(ctx->ka);

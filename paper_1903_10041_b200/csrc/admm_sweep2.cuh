@@ -8,9 +8,10 @@
 //    owning whole work units (a scenario row j, or a segment of a long row)
 //    in a fixed order: deterministic;
 //  * every warp streams its own chunks of 64 cells (chunk c of a unit belongs
-//    to warp c mod 4) HBM -> shared memory with 1-D TMA bulk copies
-//    (cp.async.bulk + mbarrier complete_tx) into a private NS-stage ring issued
-//    by its lane 0: the fp64 work of chunk c overlaps the HBM reads of the
+//    to warp c mod 4) HBM -> shared memory with three or four TMA tensor copies
+//    (cp.async.bulk.tensor: x of every source as one 3-D box, a2/a1/b2/b1 of
+//    every source as one 4-D box, y and v as one, the box bounds as one; mbarrier
+//    complete_tx) into a private NS-stage ring issued by its lane 0: the fp64 work of chunk c overlaps the HBM reads of the
 //    warp's next chunks without holding registers for loads in flight, and no
 //    warp ever waits for another one (no barrier, no shared ring);
 //  * two cells per thread: Gauss-Seidel over the sources (6a) with Algorithm 1
@@ -26,6 +27,8 @@
 //    and the residual maxima are reduced by the last CTA in CTA order, which
 //    also runs the check / rho adaptation and writes the next control block.
 #pragma once
+#include <cuda.h>
+
 #include "admm_kernels.cuh"
 
 namespace admm_dev {
@@ -40,7 +43,16 @@ struct S2Args {
 
 constexpr int S2_NT = 128;  // threads per CTA
 constexpr int S2_NW = S2_NT / 32;
-constexpr int S2_UB = 4;    // unit slots of the row partials (flow-controlled by s_gen)
+constexpr int S2_UB = 8;    // unit slots of the row partials (flow-controlled by s_gen)
+
+// TMA tensor maps of the arrays a sweep streams (built by the host, admm.cu plan_stream):
+//   x   [m][q][n_pad] fp64, box {TL, 1, M}
+//   c   [4][m][q][n_pad] (a2, a1, b2, b1 at one stride; fp64, or the fp32 copies), box {TL, 1, M, 4}
+//   yv  [2][q][n_pad] (y, v adjacent) fp64, box {TL, 1, 2}
+//   box [2][m][n_pad] (lo, hi adjacent) fp64, box {TL, M, 2} (BX layout only)
+struct S2Maps {
+    CUtensorMap x, c, yv, box;
+};
 
 // one stage of a warp's ring (chunk of TL = 32 L cells, L cells per lane): x_i (M, fp64),
 // y, v (fp64), a2_i, a1_i, b2_i, b1_i (CT), and with BX the box lo_i, hi_i (fp64: horizon-
@@ -49,42 +61,44 @@ constexpr int S2_UB = 4;    // unit slots of the row partials (flow-controlled b
 template <int M, typename CT, int L, bool BX>
 struct S2Cfg {
     static constexpr int TL = 32 * L;
-    static constexpr int YOFF = M * TL * 8;
-    static constexpr int VOFF = (M + 1) * TL * 8;
-    static constexpr int COFF = (M + 2) * TL * 8;
-    static constexpr int BOFF = COFF + 4 * M * TL * (int)sizeof(CT);
+    static constexpr int YOFF = M * TL * 8;          // x: [M][TL]
+    static constexpr int VOFF = (M + 1) * TL * 8;    // y, v: [2][TL]
+    static constexpr int COFF = (M + 2) * TL * 8;    // coefficient c of source i: [4][M][TL]
+    static constexpr int CSTR = M * TL * (int)sizeof(CT);  // bytes between coefficients
+    static constexpr int BOFF = COFF + 4 * CSTR;     // lo, hi: [2][M][TL]
     static constexpr int STAGE = BOFF + (BX ? 2 * M * TL * 8 : 0);
+    static constexpr unsigned BYTES = (unsigned)((M + 2 + (BX ? 2 * M : 0)) * TL * 8 + 4 * CSTR);
 };
 
 __device__ __forceinline__ unsigned s2_smem(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void s2_bar_init(unsigned long long* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2_smem(bar)) : "memory");
+// shared-memory operands are passed as 32-bit shared addresses computed once (the
+// conversion inside a polling loop would be redone on every try)
+__device__ __forceinline__ void s2_bar_init(unsigned bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void s2_expect(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s2_smem(bar)), "r"(bytes)
-                 : "memory");
+__device__ __forceinline__ void s2_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ bool s2_try(unsigned long long* bar, unsigned phase) {
+__device__ __forceinline__ bool s2_try(unsigned bar, unsigned phase) {
     unsigned ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(s2_smem(bar)), "r"(phase)
+        : "r"(bar), "r"(phase)
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void s2_wait(unsigned long long* bar, unsigned phase) {
+__device__ __forceinline__ void s2_wait(unsigned bar, unsigned phase) {
     while (!s2_try(bar, phase)) {
     }
 }
-__device__ __forceinline__ void s2_tma(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+__device__ __forceinline__ void s2_tma(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            s2_smem(dst)),
-        "l"(src), "r"(bytes), "r"(s2_smem(bar))
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
 
@@ -128,40 +142,32 @@ struct S2Pos {
     }
 };
 
+__device__ __forceinline__ void s2_tmap3(unsigned dst, const CUtensorMap* m, int c0, int c1, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(0), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void s2_tmap4(unsigned dst, const CUtensorMap* m, int c0, int c1, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            dst),
+        "l"(m), "r"(c0), "r"(c1), "r"(0), "r"(0), "r"(bar)
+        : "memory");
+}
+
+// one chunk (row j, chunk t) into a stage: three tensor copies (four with the box); a
+// chunk past n_pad is zero-filled by the TMA unit and counts its full box
 template <int M, typename CT, int L, bool BX>
-__device__ __forceinline__ void s2_issue(const KArgs& a, long long j, int t, unsigned char* st,
-                                         unsigned long long* bar) {
+__device__ __forceinline__ void s2_issue(const S2Maps& tm, long long j, int t, unsigned st, unsigned bar) {
     using C = S2Cfg<M, CT, L, BX>;
-    constexpr int TL = C::TL;
-    const int k0 = t * TL;
-    const int nc = min(TL, a.n_pad - k0);  // n_pad % 4 == 0: byte counts are multiples of 16
-    const unsigned b8 = (unsigned)nc * 8u, bc = (unsigned)nc * (unsigned)sizeof(CT);
-    s2_expect(bar, (unsigned)(M + 2 + (BX ? 2 * M : 0)) * b8 + 4u * M * bc);
-    const long long qn = a.q * (long long)a.n_pad;
-    const long long row = j * a.n_pad + k0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) s2_tma(st + (size_t)i * TL * 8, a.x + i * qn + row, b8, bar);
-    if constexpr (BX) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            s2_tma(st + C::BOFF + (size_t)(2 * i) * TL * 8, a.lo + (long long)i * a.n_pad + k0, b8, bar);
-            s2_tma(st + C::BOFF + (size_t)(2 * i + 1) * TL * 8, a.hi + (long long)i * a.n_pad + k0, b8, bar);
-        }
-    }
-    s2_tma(st + C::YOFF, a.y + row, b8, bar);
-    s2_tma(st + C::VOFF, a.v + row, b8, bar);
-    const CT* src[4];
-    if constexpr (sizeof(CT) == 4) {
-        src[0] = a.fa2; src[1] = a.fa1; src[2] = a.fb2; src[3] = a.fb1;
-    } else {
-        src[0] = reinterpret_cast<const CT*>(a.a2); src[1] = reinterpret_cast<const CT*>(a.a1);
-        src[2] = reinterpret_cast<const CT*>(a.b2); src[3] = reinterpret_cast<const CT*>(a.b1);
-    }
-#pragma unroll
-    for (int i = 0; i < M; ++i)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            s2_tma(st + C::COFF + (size_t)(4 * i + c) * TL * sizeof(CT), src[c] + i * qn + row, bc, bar);
+    const int k0 = t * C::TL;
+    s2_expect(bar, C::BYTES);
+    s2_tmap3(st, &tm.x, k0, (int)j, bar);
+    s2_tmap4(st + C::COFF, &tm.c, k0, (int)j, bar);
+    s2_tmap3(st + C::YOFF, &tm.yv, k0, (int)j, bar);
+    if constexpr (BX) s2_tmap3(st + C::BOFF, &tm.box, k0, 0, bar);
 }
 
 // L consecutive values of a shared-memory stream (fp64 or fp32), widened
@@ -193,7 +199,8 @@ __device__ __forceinline__ void s2_stL(double* p, const double* v) {
 // staged (BX): horizon-type problems (few rows, M up to 4) -- half the registers per lane,
 // so more warps per SM, and no L1 misses on the box
 template <int M, int MODE, typename CT, int NS, int L, bool BX>
-__global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)) sweep2_kernel(KArgs a, S2Args s) {
+__global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2))
+    sweep2_kernel(KArgs a, S2Args s, const __grid_constant__ S2Maps tm) {
     using C = S2Cfg<M, CT, L, BX>;
     constexpr int TL = C::TL;
     extern __shared__ __align__(128) unsigned char s2_sm[];
@@ -238,18 +245,19 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
         s_cons[tid / M][2][tid % M] = INFINITY;
     }
     if (tid < S2_NW * NS) {
-        s2_bar_init(&s_full[0][0] + tid);
+        s2_bar_init(s2_smem(&s_full[0][0] + tid));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     unsigned char* const ring = s2_sm + (size_t)wid * NS * C::STAGE;  // this warp's stages
+    const unsigned ring_s = s2_smem(ring), bar_s = s2_smem(&s_full[wid][0]);
     S2Pos ahead;  // this warp's chunk NS positions ahead of the consumer: the refill of its stage
     ahead.u = blockIdx.x;
     ahead.lu = 0;
     ahead.set(s, wid);
     for (int st = 0; st < NS && ahead.u < s.U; ++st) {
-        if (lane == 0) s2_issue<M, CT, L, BX>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+        if (lane == 0) s2_issue<M, CT, L, BX>(tm, ahead.j, ahead.c, ring_s + st * C::STAGE, bar_s + 8 * st);
         ahead.next(s, wid);
     }
 
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
         for (int c = cs + s2_first(wid, (unsigned)unit); c < ce; c += S2_NW) {
             const int k = c * TL + L * lane;  // first of this thread's L cells
             const unsigned char* sp = ring + (size_t)st * C::STAGE;
-            s2_wait(&s_full[wid][st], ph);
+            s2_wait(bar_s + 8 * st, ph);
             if (k < a.n_pad) {
                 const bool k0 = (k == 0) && a.k0own;
                 bool vc[L];
@@ -329,15 +337,15 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
                 // ---- (6a) Gauss-Seidel over sources (same arithmetic as gs_cellU)
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i) * TL * sizeof(CT) +
+                    const unsigned char* cp = sp + C::COFF + (size_t)i * TL * sizeof(CT) +
                                               L * sizeof(CT) * lane;
                     double a2[L], a1[L], b2[L], b1[L];
                     s2_ldL<CT, L>(cp, a2);
-                    s2_ldL<CT, L>(cp + TL * sizeof(CT), a1);
+                    s2_ldL<CT, L>(cp + C::CSTR, a1);
                     double Cq[L], Dq[L], bn[L], cn[L], dn[L], lo[L], hi[L];
                     if constexpr (BX) {
-                        s2_ldL<double, L>(sp + C::BOFF + (size_t)(2 * i) * TL * 8 + 8 * L * lane, lo);
-                        s2_ldL<double, L>(sp + C::BOFF + (size_t)(2 * i + 1) * TL * 8 + 8 * L * lane, hi);
+                        s2_ldL<double, L>(sp + C::BOFF + (size_t)i * TL * 8 + 8 * L * lane, lo);
+                        s2_ldL<double, L>(sp + C::BOFF + (size_t)(M + i) * TL * 8 + 8 * L * lane, hi);
                     } else if constexpr (L == 2) {
                         const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
                         const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
@@ -375,8 +383,8 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
                         }
                         continue;
                     }
-                    s2_ldL<CT, L>(cp + 2 * TL * sizeof(CT), b2);
-                    s2_ldL<CT, L>(cp + 3 * TL * sizeof(CT), b1);
+                    s2_ldL<CT, L>(cp + 2 * C::CSTR, b2);
+                    s2_ldL<CT, L>(cp + 3 * C::CSTR, b1);
                     bool allq = true, anyq = false;
 #pragma unroll
                     for (int u = 0; u < L; ++u) {
@@ -434,11 +442,11 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
                 // ---- row partials: exact fixed point, dg extrema on checks
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    const unsigned char* cp = sp + C::COFF + (size_t)(4 * i + 2) * TL * sizeof(CT) +
+                    const unsigned char* cp = sp + C::COFF + 2 * C::CSTR + (size_t)i * TL * sizeof(CT) +
                                               L * sizeof(CT) * lane;
                     double b2[L], b1[L];
                     s2_ldL<CT, L>(cp, b2);
-                    s2_ldL<CT, L>(cp + TL * sizeof(CT), b1);
+                    s2_ldL<CT, L>(cp + C::CSTR, b1);
 #pragma unroll
                     for (int u = 0; u < L; ++u)
                         if (!vc[u]) xn[i][u] = 0.0;  // padding stays 0
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
             if (lane == 0 && ahead.u < s.U) {
                 // refill the stage with this warp's chunk NS positions ahead
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                s2_issue<M, CT, L, BX>(a, ahead.j, ahead.c, ring + (size_t)st * C::STAGE, &s_full[wid][st]);
+                s2_issue<M, CT, L, BX>(tm, ahead.j, ahead.c, ring_s + st * C::STAGE, bar_s + 8 * st);
             }
             ahead.next(s, wid);
             if (++st == NS) {
@@ -483,8 +491,7 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
         // the last warp to arrive finalises
         const int b = (int)(unit & (S2_UB - 1));
         if (lane == 0)
-            while (*(volatile unsigned*)&s_gen[b] != (unsigned)(unit >> 2)) {
-            }
+            while (*(volatile unsigned*)&s_gen[b] != (unsigned)(unit / S2_UB)) __nanosleep(64);
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < M; ++i) {

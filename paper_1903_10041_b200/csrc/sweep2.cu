@@ -44,9 +44,9 @@ const void* sweep2_pick(int m, int mode, int coeff_bytes, long long q, int* ns, 
     return nullptr;
 }
 
-// Units = (row, segment of TPS tiles).  Whole rows (S = 1) unless splitting rows
+// Units = (row, segment of TPS chunks).  Whole rows (S = 1) unless splitting rows
 // balances the CTAs better: the estimated time of a split is the largest unit count
-// of a CTA x its tiles per unit (+2 % per extra segment for the global row atomics).
+// of a CTA x (its chunks per unit + a fixed per-unit cost).
 S2Args sweep2_plan(long long q, long long n_pad, int tl, int g_max) {
     S2Args s{};
     s.TPR = (int)((n_pad + tl - 1) / tl);
@@ -57,7 +57,9 @@ S2Args sweep2_plan(long long q, long long n_pad, int tl, int g_max) {
         if ((s.TPR + tps - 1) / tps != S) continue;  // not a distinct split
         const long long U = q * S;
         const long long G = std::min<long long>(U, g_max);
-        const double t = (double)((U + G - 1) / G) * tps * (1.0 + 0.02 * (S > 1));
+        // + ~3 chunks of fixed cost per unit (row scalars, finalisation, row atomics):
+        // measured at q = 1e3 (S = 1 / 2 / 4: 35 / 30 / 26 % of the HBM peak)
+        const double t = (double)((U + G - 1) / G) * (tps + 3.0);
         if (t < best * 0.98) {
             best = t;
             best_S = S;

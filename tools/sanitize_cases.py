@@ -6,14 +6,21 @@ import paper_1903_10041_b200 as L, synth
 
 cases = [("toy", synth.toy_problem()), ("phev q3 n200", synth.phev_problem(200, 3)),
          ("random m3 n37 q3", synth.random_problem(3, 37, 3, seed=5)),
-         ("random m2 n1025 q2", synth.random_problem(2, 1025, 2, seed=6))]
+         ("random m2 n1025 q2", synth.random_problem(2, 1025, 2, seed=6)),
+         # more rows than CTAs and rows of several chunks/tiles: every CTA walks several units
+         # (the row loop's and the TMA sweep's slot reuse)
+         ("phev q1200 n300", synth.phev_problem(300, 1200))]
 engines = [("stream", 1, {}), ("cluster", 2, {}), ("grid", 2, {"ADMM_PERSIST_GRID": "1"}),
-           ("stream_fx", 1, {"ADMM_SWEEP_FX": "1"}), ("stream_tma", 1, {"ADMM_STREAM_TMA": "1"}),
-           ("stream_rl", 1, {"ADMM_SWEEP_RL": "1"}), ("stream_u4", 1, {"ADMM_SWEEP_CPT": "4"}),
-           ("stream_pf", 1, {"ADMM_SWEEP_PF": "1"}),
-           ("stream_rl_f32", 1, {"ADMM_SWEEP_RL": "1"})]
-KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_STREAM_TMA", "ADMM_SWEEP_RL", "ADMM_SWEEP_CPT",
-        "ADMM_SWEEP_PF")
+           ("stream_l1", 1, {"ADMM_S2_L": "1"}), ("stream_l2", 1, {"ADMM_S2_L": "2"}),
+           ("stream_f32", 1, {}),
+           ("stream_legacy", 1, {"ADMM_SWEEP2": "0"}),
+           ("stream_fx", 1, {"ADMM_SWEEP_FX": "1", "ADMM_SWEEP2": "0"}),
+           ("stream_rl", 1, {"ADMM_SWEEP_RL": "1", "ADMM_SWEEP2": "0"}),
+           ("stream_u4", 1, {"ADMM_SWEEP_CPT": "4", "ADMM_SWEEP2": "0"}),
+           ("stream_pf", 1, {"ADMM_SWEEP_PF": "1", "ADMM_SWEEP2": "0"}),
+           ("stream_rl_f32", 1, {"ADMM_SWEEP_RL": "1", "ADMM_SWEEP2": "0"})]
+KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2", "ADMM_S2_L", "ADMM_SWEEP_RL",
+        "ADMM_SWEEP_CPT", "ADMM_SWEEP_PF")
 only = os.environ.get("ENGINES")
 for name, P in cases:
     for en, mode, env in engines:
