@@ -75,14 +75,31 @@ def parse():
     return ap.parse_args()
 
 
-def _shard_range():
+def _dist_module():
     """paper_1903_10041_b200/dist.py loaded by path: the reference arm must not import
     the product package (its __init__ loads the CUDA library)."""
     spec = importlib.util.spec_from_file_location(
         "_admm_dist", os.path.join(ROOT, "paper_1903_10041_b200", "dist.py"))
     m = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(m)
-    return m.shard_range
+    return m
+
+
+def _shard_range():
+    return _dist_module().shard_range
+
+
+def _horizon_slice(P, k0, k1):
+    """Steps [k0, k1) of every array of a problem (horizon blocks)."""
+    import numpy as np
+
+    Q = dict(P)
+    for k in ("a2", "a1", "a0", "b2", "b1", "b0"):
+        Q[k] = np.ascontiguousarray(P[k][:, :, k0:k1])
+    for k in ("lo", "hi", "y"):
+        Q[k] = np.ascontiguousarray(P[k][:, k0:k1])
+    Q["n"] = k1 - k0
+    return Q
 
 
 # ------------------------------------------------------------------ workloads
@@ -124,12 +141,16 @@ def workload(args, rank, world):
                     cfg="configs[0]", scaling="weak",
                     name="nominal toy n=10 m=2 q=1, 200 fixed iterations (BASELINE.json configs[0])")
     if w == "horizon":
+        # N > 1: horizon blocks (rank r owns a balanced range of the n steps; strong scaling)
         n = args.n or 1_000_000
         P = synth.horizon_problem(n)
-        return dict(kind="solve", m=4, n=n, q_total=1, j0=0, j1=1, make=lambda a, q: P,
+        k0, k1 = _dist_module().horizon_range(n, rank, world) if world > 1 else (0, n)
+        make = (lambda a, q: P) if world == 1 else (lambda a, q: _horizon_slice(P, k0, k1))
+        return dict(kind="solve", m=4, n=n, q_total=1, j0=0, j1=1, make=make, k0=k0, k1=k1,
                     r_bar=1e-6 * P["c"][2], sigma_bar=1e-2, max_iter=20000, cfg="configs[2]",
-                    scaling="weak",
-                    name=f"horizon sweep m=4 q=1 n={n}, solve to tol (BASELINE.json configs[2])")
+                    scaling="strong" if world > 1 else "weak", horizon_blocks=world > 1,
+                    name=f"horizon sweep m=4 q=1 n={n}, solve to tol (BASELINE.json configs[2])"
+                         + (f", horizon blocks over {world} GPUs" if world > 1 else ""))
     raise ValueError(w)
 
 
@@ -272,6 +293,7 @@ def run_ours(args, W, rank, world, local_rank, dist=None, steps=None, warmup=Non
     m, n, q_total = W["m"], W["n"], W["q_total"]
     H = _pinned_problem(W)
     q_loc = H["q"]
+    n_loc = W.get("k1", n) - W.get("k0", 0)
     s = L.AdmmSolver(m, n, q_total, device=local_rank, dist=dist, r_bar=W["r_bar"],
                      sigma_bar=W["sigma_bar"], coeff_bits=args.coeff_bits, exec_mode=args.exec)
     s.set_problem_packed(H["f"], H["g"], H["lo"], H["hi"], H["y"], H["c"])
@@ -320,7 +342,7 @@ def run_ours(args, W, rank, world, local_rank, dist=None, steps=None, warmup=Non
     res = dict(value=elem * tot_iters / T, it_per_s=tot_iters / T, T=T, iters=iters,
                step_ms=step_ms, clocks=clk.summary(local_rank), engine=kname,
                gpu_launches=int(launches1 - launches0))
-    res["roof"] = roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms)
+    res["roof"] = roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms, n_loc)
     if e2e and not args.no_e2e:
         res["e2e"] = run_e2e(s, W, H, dev, flush, world, steps, warmup)
     s.close()
@@ -328,7 +350,7 @@ def run_ours(args, W, rank, world, local_rank, dist=None, steps=None, warmup=Non
     return res
 
 
-def roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms):
+def roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms, n_loc=None):
     """Dominant kernel's roofline.  Streaming engines (1, 4): one launch = one ADMM
     iteration, HBM-bound: achieved = algorithmic bytes per iteration / measured time
     per launch.  On-chip engines (2, 3): one launch = the whole call with the state
@@ -337,7 +359,7 @@ def roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms):
     import numpy as np
 
     m, n = W["m"], W["n"]
-    ab = alg_bytes_per_iter(m, n, q_loc, args.coeff_bits)
+    ab = alg_bytes_per_iter(m, n if n_loc is None else n_loc, q_loc, args.coeff_bits)
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs")
     peak = hbm if hbm else 6650.0
@@ -373,7 +395,7 @@ def run_e2e(s, W, H, dev, flush, world, steps, warmup):
     set_problem_packed (H2D of every input) -> iterate/solve -> solution (D2H)."""
     import torch
 
-    x = torch.empty((W["m"], H["q"], W["n"]), dtype=torch.float64).pin_memory()
+    x = torch.empty((W["m"], H["q"], W.get("k1", W["n"]) - W.get("k0", 0)), dtype=torch.float64).pin_memory()
     x1 = torch.empty(W["m"], dtype=torch.float64).pin_memory()
     stream = torch.cuda.current_stream(dev)
 
@@ -677,7 +699,8 @@ def config_of(args, W, world):
     cfg = {"workload": W["name"], "baseline_config": W["cfg"],
            "l2": "flushed (512 MiB write) before each timed step; inputs > L2",
            "coeff_bits": args.coeff_bits,
-           "parallelism": f"scenario-sharded dp{world}" if world > 1 else "1 GPU"}
+           "parallelism": (f"horizon blocks x{world}" if W.get("horizon_blocks") else
+                           f"scenario-sharded dp{world}") if world > 1 else "1 GPU"}
     if W["kind"] != "quartic":
         cfg.update(m=W["m"], n=W["n"], q_total=W["q_total"])
     return cfg
@@ -729,7 +752,7 @@ def main():
     if world > 1 and W["kind"] != "quartic":
         import paper_1903_10041_b200 as L
 
-        dist = L.make_dist(W["q_total"])
+        dist = L.make_dist(W["q_total"], horizon=W["n"] if W.get("horizon_blocks") else None)
     res = run_ours(args, W, rank, world, local_rank, dist=dist)
     metric, unit = metric_of(W)
     line = {
@@ -741,9 +764,11 @@ def main():
         "config": config_of(args, W, world),
         "gpu_launches": res["gpu_launches"], "roofline": res["roof"],
     }
-    line["config"]["engine"] = res["engine"]
+    # config is the workload only (identical in the reference arm's line); what ran and how
+    # many iterations each step took are reported beside it
+    line["engine"] = res["engine"]
     if W["kind"] != "quartic":
-        line["config"]["iterations_per_step"] = res["iters"]
+        line["iterations_per_step"] = res["iters"]
         line["iterations_per_s"] = res["it_per_s"]
     if "e2e" in res:
         line["e2e"] = res["e2e"]

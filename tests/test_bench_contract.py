@@ -86,3 +86,39 @@ def test_reference_arm_default_workload_loads_no_product_code():
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     assert d["config"]["q_total"] == 100000 and d["config"]["baseline_config"] == "configs[3]"
     assert "q_total = 100000" in d["cpu_baseline"]["sample"]
+
+
+def test_horizon_workload_blocks_at_n_gpus():
+    """--workload horizon at N > 1 uses horizon blocks: rank r's problem is its balanced
+    range [k0, k1) of the steps of the same synthetic instance (the slices tile the
+    horizon), and the roofline's byte model counts the rank's own steps."""
+    import argparse
+
+    import numpy as np
+
+    b = _bench()
+    args = argparse.Namespace(workload="horizon", n=1001, q=None, family="C", coeff_bits=64)
+    full = b.workload(args, 0, 1)["make"](0, 1)
+    parts = []
+    for r in range(3):
+        W = b.workload(args, r, 3)
+        assert W["horizon_blocks"] and W["scaling"] == "strong"
+        P = W["make"](0, 1)
+        assert P["n"] == W["k1"] - W["k0"] and P["a2"].shape == (4, 1, P["n"])
+        parts.append(P)
+    for key in ("a2", "b2", "b1"):
+        assert np.array_equal(np.concatenate([p[key] for p in parts], axis=2), full[key])
+    for key in ("lo", "hi", "y"):
+        assert np.array_equal(np.concatenate([p[key] for p in parts], axis=1), full[key])
+
+
+def test_reference_and_our_config_are_the_same_workload():
+    """The driver compares the two arms' `config`: both are built by config_of from
+    the same workload description (no engine / timing keys inside)."""
+    import argparse
+
+    b = _bench()
+    args = argparse.Namespace(workload="toy", n=None, q=None, family="C", coeff_bits=64)
+    W = b.workload(args, 0, 1)
+    ref = _reference_line("toy")
+    assert ref["config"] == b.config_of(args, W, 1)

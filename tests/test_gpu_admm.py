@@ -494,3 +494,35 @@ def test_phev_q200_iteration_count_matches_oracle_record():
     assert rec["status"] == 0 and ig["converged"]
     assert abs(ig["iterations"] - rec["iterations"]) <= prm["check_every"], (ig["iterations"], rec["iterations"])
     assert abs(ig["objective"] - rec["objective"]) <= 1e-6 * abs(rec["objective"])
+
+
+@pytest.mark.parametrize("env", [{}, {"ADMM_S2_L": "1"}], ids=["two_cells", "one_cell_box"])
+def test_streaming_engine_bitwise_deterministic(env):
+    """include/admm.h: same inputs, params and world size give bitwise-identical
+    results.  The TMA sweep's row sums are exact integers, its consensus partials are
+    combined in a fixed warp / CTA order: two runs of 100 iterations (10 checks with
+    rho adaptation) on a problem with more rows than CTAs agree bit for bit in every
+    state array and in the residual history."""
+    import os
+
+    L = _lib()
+    P = synth.phev_problem(700, 1500)
+    out = []
+    for _ in range(2):
+        for k in _ENV_KEYS:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        try:
+            s = L.AdmmSolver(2, 700, 1500, r_bar=1e-6 * P["c"][1], exec_mode=1)
+            s.set_problem(P)
+            s.iterate(100)
+            out.append((s.state(), s.history(), L._lib.ENGINE_NAMES.get(s.engine()[0])))
+            s.close()
+        finally:
+            for k in _ENV_KEYS:
+                os.environ.pop(k, None)
+    (S0, h0, e0), (S1, h1, e1) = out
+    assert e0 == e1 == "sweep2_kernel"
+    for k in STATE_KEYS:
+        assert np.array_equal(S0[k], S1[k]), k
+    assert np.array_equal(h0, h1)
