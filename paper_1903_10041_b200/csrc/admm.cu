@@ -30,6 +30,11 @@
 #include "admm_persist.cuh"
 #include "admm_onchip.cuh"
 #include "admm_sweep2.cuh"
+#include "admm_onchip2.cuh"
+
+namespace admm_dev {
+const void* cluster2_pick(int m, int mode);  // onchip2.cu
+}
 
 using namespace admm_dev;
 
@@ -43,7 +48,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Layout {
     size_t a2, a1, a0, b2, b1, b0, lo, hi, y, c, sb0, x, v, lam, zeta, h, p, nu, cta_part,
         row_part, obj_rows, xsend, xall, hist, row_cnt, glob_cnt, ctrl, iter, prm, vflag, pg, pc, pr,
-        prc, pbar, pub, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, cf, hzdg, hzrow, total;
+        prc, pbar, pub, pub2, chkv2, chkx2, cnt2, xraw, bq, ib2s, chk, gbound, rowacc, rowdg, rowcnt, cf, hzdg, hzrow, total;
 };
 
 // streaming sweep block size: 2 cells per thread, at most ADMM_SWEEP_BS (default
@@ -95,6 +100,11 @@ Layout make_layout(int m, long long n, long long q, int sms) {
     L.prc = take(2 * (size_t)m * std::min<size_t>(q, GP) * 4 * 8);
     L.pbar = take(64 * 4);
     L.pub = take((size_t)PUB_BUFS * m * std::min<size_t>(q, GP) * 8);
+    // message-passing cluster engine: LL publication buffers (16 B per value)
+    L.pub2 = take((size_t)OC2_BUFS * m * std::min<size_t>(q, GP) * 16);
+    L.chkv2 = take((size_t)OC2_BUFS * OC2_CHKV * std::min<size_t>(q, GP) * 16);
+    L.chkx2 = take((size_t)OC2_BUFS * m * std::min<size_t>(q, GP) * 16);
+    L.cnt2 = take(16);
     L.xraw = take(2 * (size_t)m * std::min<size_t>(q, GP) * 8);
     // prepared constants for the on-chip engine (only for problems that can be on chip)
     const bool onchip_sized = (size_t)m * q * n_pad <= ONCHIP_PREP_MAX_ELEMS;
@@ -504,6 +514,7 @@ struct admm_ctx {
     unsigned long long cond = 0;  // cudaGraphConditionalHandle
     bool no_graph = false;        // ADMM_NO_GRAPH=1: plain launches (for ncu)
     int last_engine = 0;          // ADMM_ENGINE_* of the last iterate/solve
+    DParams dparams{};            // parameters of the current call (host copy of the device block)
     long long launches = 0;       // kernels launched by this context since create
     bool prep_ok = false;         // bq / ib2s valid (on-chip-sized problems)
     bool fx_ok = false;           // fixed-point scales of the row sums valid (finite bounds)
@@ -559,7 +570,8 @@ void upload_params(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     d.rescale = ctx->params.rescale_duals;
     d.box_mode = ctx->params.box_mode;
     d.stop_on_conv = stop_on_conv;
-    cudaMemcpyAsync(ctx->ws + ctx->L.prm, &d, sizeof(d), cudaMemcpyHostToDevice, ctx->stream);
+    ctx->dparams = d;
+    cudaMemcpyAsync(ctx->ws + ctx->L.prm, &ctx->dparams, sizeof(d), cudaMemcpyHostToDevice, ctx->stream);
 }
 
 // F2: round a2, a1, b2, b1 to fp32 (round to nearest even, the cast), keep the
@@ -1058,34 +1070,198 @@ admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
     return ADMM_OK;
 }
 
+// Message-passing cluster engine (admm_onchip2.cuh): rows in clusters of T CTAs of nw
+// warps (tile 0: nw-1 bulk warps + the consensus warp).  The plan minimises a model of
+// the iteration time over (T, nw) among the shapes whose q*T CTAs are all co-resident:
+//   cells per thread k_t = ceil(cells of tile t / bulk threads of tile t) -> latency
+//   L * max_t k_t of the dependent Algorithm-1 chains, and fp64 throughput
+//   W * (CTAs per SM) * (cells per CTA) when an SM holds several CTAs,
+// plus a per-message cost of the row exchange (T * nw slots summed by the row warp).
+// L = 2800 and W = 6.9 cycles are the PHEV q = 50 per-cell latency and per-SM
+// throughput of profiles/r02b/cluster_phase.txt.  ADMM_CLUSTER_T / ADMM_CLUSTER_WARPS
+// force a shape (experiments).
+struct C2Plan {
+    bool ok = false;
+    int T = 0, NW = 0, TC0 = 0, TC = 0, G = 0;
+    size_t smem = 0;
+    long long key_q = -1, key_n = -1;
+    int key_m = -1, key_mode = -1;
+};
+
+size_t oc2_smem(int m, long long TCM, int T, int nw) {
+    return ((((size_t)(9 * m + 2) * TCM + 1) & ~(size_t)1) * 8) + oc2_msg_bytes(m, T, nw);
+}
+
+C2Plan plan_cluster2(admm_ctx* ctx, const void* fn) {
+    C2Plan pl;
+    if (ctx->dist || !fn || !ctx->prep_ok || !ctx->fx_ok) return pl;
+    const long long n = ctx->n, q = ctx->q;
+    const int sms = ctx->sms, m = ctx->m;
+    if (q > 32LL * sms) return pl;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        cudaGetLastError();
+    int forceT = 0, forceW = 0;
+    if (const char* e = getenv("ADMM_CLUSTER_T")) forceT = atoi(e);
+    if (const char* e = getenv("ADMM_CLUSTER_WARPS")) forceW = atoi(e);
+    struct Cand {
+        double cost;
+        int T, NW;
+        long long TC0, TC;
+    };
+    std::vector<Cand> cand;
+    for (int T = 1; T <= OC2_MAX_T; ++T) {
+        if (forceT && T != forceT) continue;
+        if (T > 1 && n < 2LL * T) break;
+        for (int NW = 2; NW <= OC2_MAX_W; ++NW) {
+            if (forceW && NW != forceW) continue;
+            const long long b0 = 32LL * (NW - 1), b1 = 32LL * NW;  // bulk threads of tile 0 / others
+            long long TC0 = n, TC = n;
+            if (T > 1) {
+                // cells in proportion to the bulk threads (tile 0 also runs the consensus chain)
+                TC0 = std::max<long long>(1, std::min<long long>(n - (T - 1), (long long)((double)n * b0 / (b0 + (T - 1) * b1))));
+                if (const char* e = getenv("ADMM_TILE0_FRAC"))
+                    TC0 = std::max<long long>(1, std::min<long long>(n - (T - 1), std::llround(atof(e) * n / T)));
+                TC = (n - TC0 + T - 2) / (T - 1);
+                if (TC0 + (T - 2) * TC >= n) continue;  // last tile would be empty
+            }
+            const long long TCM = std::max(TC0, TC);
+            if (oc2_smem(m, TCM, T, NW) > 200 * 1024) continue;
+            const long long G = q * T;
+            const long long k = std::max((TC0 + b0 - 1) / b0, (TC + b1 - 1) / b1);  // cells per thread
+            // CTAs per SM: register file (128 regs x 32 lanes per warp) and shared memory
+            const long long by_regs = 64 / NW, by_smem = (228 * 1024) / (long long)(oc2_smem(m, TCM, T, NW) + 1024);
+            const long long per_sm_cap = std::max(1LL, std::min(by_regs, by_smem));
+            const long long cps = (G + sms - 1) / sms;
+            if (cps > per_sm_cap) continue;
+            const double L = 2800.0 * m / 2.0, W = 6.9 * m / 2.0;
+            const double cost = std::max(L * (double)k, W * (double)(cps * TCM)) + 30.0 * ((T * NW + 31) / 32) +
+                                40.0 * T;
+            cand.push_back({cost, T, NW, TC0, TC});
+        }
+    }
+    std::sort(cand.begin(), cand.end(), [](const Cand& x, const Cand& y) {
+        return x.cost < y.cost || (x.cost == y.cost && (x.T < y.T || (x.T == y.T && x.NW < y.NW)));
+    });
+    for (const Cand& c : cand) {
+        const long long TCM = std::max(c.TC0, c.TC);
+        const size_t smem = oc2_smem(m, TCM, c.T, c.NW);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(q * c.T));
+        cfg.blockDim = dim3((unsigned)(32 * c.NW));
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c.T;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if ((long long)nclusters < q) continue;  // all CTAs must be co-resident
+        if (getenv("ADMM_DEBUG_PLAN"))
+            fprintf(stderr, "[admm] cluster2 plan: T=%d NW=%d TC0=%lld TC=%lld G=%lld smem=%zu cost=%.0f clusters=%d\n",
+                    c.T, c.NW, c.TC0, c.TC, q * c.T, smem, c.cost, nclusters);
+        pl.ok = true;
+        pl.T = c.T;
+        pl.NW = c.NW;
+        pl.TC0 = (int)c.TC0;
+        pl.TC = (int)c.TC;
+        pl.G = (int)(q * c.T);
+        pl.smem = smem;
+        return pl;
+    }
+    return pl;
+}
+
+admm_status launch_cluster2(admm_ctx* ctx, const void* fn, const C2Plan& pl) {
+    C2Args ca;
+    ca.TC0 = pl.TC0;
+    ca.TC = pl.TC;
+    ca.T = pl.T;
+    ca.G = pl.G;
+    for (int i = 0; i < MAXM; ++i) {
+        ca.fx_scale[i] = ctx->fx_scale[i];
+        ca.fx_inv[i] = ctx->fx_inv[i];
+    }
+    ca.bq = (const double*)(ctx->ws + ctx->L.bq);
+    ca.ib2s = (const double*)(ctx->ws + ctx->L.ib2s);
+    ca.pub = (unsigned long long*)(ctx->ws + ctx->L.pub2);
+    ca.chkv = (unsigned long long*)(ctx->ws + ctx->L.chkv2);
+    ca.chkx = (unsigned long long*)(ctx->ws + ctx->L.chkx2);
+    ca.cnt = (unsigned*)(ctx->ws + ctx->L.cnt2);
+    ca.prm = ctx->dparams;
+    // the same expressions as check_decide (admm_kernels.cuh), evaluated once
+    ca.thr_hi = ctx->params.hi_ratio * ctx->params.r_bar / ctx->params.sigma_bar;
+    ca.thr_lo = ctx->params.lo_ratio * ctx->params.r_bar / ctx->params.sigma_bar;
+    // epochs and check counts restart every call: clear the publication buffers, key
+    // sets and counter (contiguous in the workspace)
+    CKC(cudaMemsetAsync(ctx->ws + ctx->L.pub2, 0, ctx->L.cnt2 + 16 - ctx->L.pub2, ctx->stream));
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) != cudaSuccess)
+        return fail(ctx, ADMM_ERR_CUDA, "cluster kernel: shared memory attribute");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl.G);
+    cfg.blockDim = dim3((unsigned)(32 * pl.NW));
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pl.T;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* args[2] = {(void*)&ctx->ka, (void*)&ca};
+    CKC(cudaLaunchKernelExC(&cfg, fn, args));
+    ctx->launches += 1;  // the cluster kernel (the memset is not a kernel of ours)
+    return ADMM_OK;
+}
+
 // run until done or iter_limit, through the graph
 admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     if (!ctx->has_problem) return fail(ctx, ADMM_ERR_STATE, "set_problem must be called first");
     admm_status st = ADMM_OK;
     PPlan pl, cpl;
+    C2Plan c2pl;
     persist_fn pfn = nullptr;
     cluster_fn cfn = nullptr;
+    const void* c2fn = nullptr;
     if (ctx->params.exec_mode != ADMM_EXEC_STREAMING) {
         const char* gm = getenv("ADMM_PERSIST_GRID");  // force the grid-barrier variant
         if (!(gm && gm[0] == '1')) {
-            cfn = pick_cluster(ctx->m, ctx->params.box_mode);
-            cpl = plan_cluster(ctx, cfn);
+            // default: the message-passing cluster engine (admm_onchip2.cuh);
+            // ADMM_CLUSTER_V=1: the barrier-based one (admm_onchip.cuh)
+            const char* cv = getenv("ADMM_CLUSTER_V");
+            if (cv && cv[0] == '1') {
+                cfn = pick_cluster(ctx->m, ctx->params.box_mode);
+                cpl = plan_cluster(ctx, cfn);
+            } else {
+                c2fn = cluster2_pick(ctx->m, ctx->params.box_mode);
+                c2pl = plan_cluster2(ctx, c2fn);
+            }
         }
-        if (!cpl.ok) {
+        if (!cpl.ok && !c2pl.ok) {
             pfn = pick_persist(ctx->m, ctx->params.box_mode);
             pl = plan_persist(ctx, pfn);
         }
-        if (!pl.ok && !cpl.ok && ctx->params.exec_mode == ADMM_EXEC_PERSISTENT)
+        if (!pl.ok && !cpl.ok && !c2pl.ok && ctx->params.exec_mode == ADMM_EXEC_PERSISTENT)
             return fail(ctx, ADMM_ERR_INVALID, "problem does not fit the persistent engine");
     }
-    if (!pl.ok && !cpl.ok) {
+    if (!pl.ok && !cpl.ok && !c2pl.ok) {
         st = build_graph(ctx);
         if (st != ADMM_OK) return st;
         if (ctx->hz && !ctx->use_tma)
             return fail(ctx, ADMM_ERR_INVALID,
                         "horizon blocks need the TMA sweep: finite boxes and m <= 4");
     }
-    ctx->last_engine = cpl.ok ? ADMM_ENGINE_CLUSTER
+    ctx->last_engine = (cpl.ok || c2pl.ok) ? ADMM_ENGINE_CLUSTER
                               : (pl.ok ? ADMM_ENGINE_GRID
                                        : (ctx->use_tma ? ADMM_ENGINE_STREAM_TMA : ADMM_ENGINE_STREAM));
     upload_params(ctx, iter_limit, stop_on_conv);
@@ -1094,7 +1270,10 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     const long long start = ctx->iter_host;
     long long graph_bodies = 0;
     CKC(cudaEventRecord(ctx->e0, ctx->stream));
-    if (cpl.ok) {
+    if (c2pl.ok) {
+        st = launch_cluster2(ctx, c2fn, c2pl);
+        if (st != ADMM_OK) return st;
+    } else if (cpl.ok) {
         st = launch_cluster(ctx, cfn, cpl);
         if (st != ADMM_OK) return st;
     } else if (pl.ok) {

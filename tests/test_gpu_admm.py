@@ -59,15 +59,17 @@ def compare_states(P, So, Sg, tol=1e-9):
 # (ADMM_SWEEP_RL=1).  Read at solver creation.
 ENGINES = ["stream", "cluster", "grid"]
 ALT_ENGINES = ["stream_l1", "stream_l2", "stream_legacy", "stream_fx", "stream_u4", "stream_pf",
-               "stream_pf2", "stream_rl"]
-_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "stream_l1": 1, "stream_l2": 1, "stream_legacy": 1, "stream_fx": 1,
+               "stream_pf2", "stream_rl", "cluster_v1", "cluster_t3w2", "cluster_t1w16"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "cluster_v1": 2, "cluster_t3w2": 2, "cluster_t1w16": 2, "stream_l1": 1, "stream_l2": 1, "stream_legacy": 1, "stream_fx": 1,
          "stream_pf": 1, "stream_pf2": 1, "stream_u4": 1, "stream_rl": 1, 0: 0}
 _LEG = {"ADMM_SWEEP2": "0"}
-_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "stream_l1": {"ADMM_S2_L": "1"}, "stream_l2": {"ADMM_S2_L": "2"},
+_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "cluster_v1": {"ADMM_CLUSTER_V": "1"},
+        "cluster_t3w2": {"ADMM_CLUSTER_T": "3", "ADMM_CLUSTER_WARPS": "2"},
+        "cluster_t1w16": {"ADMM_CLUSTER_T": "1", "ADMM_CLUSTER_WARPS": "16"}, "stream_l1": {"ADMM_S2_L": "1"}, "stream_l2": {"ADMM_S2_L": "2"},
         "stream_legacy": _LEG, "stream_fx": {"ADMM_SWEEP_FX": "1", **_LEG},
         "stream_pf": {"ADMM_SWEEP_PF": "1", **_LEG}, "stream_pf2": {"ADMM_SWEEP_PF": "2", **_LEG},
         "stream_u4": {"ADMM_SWEEP_CPT": "4", **_LEG}, "stream_rl": {"ADMM_SWEEP_RL": "1", **_LEG}}
-_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_SWEEP_FX", "ADMM_SWEEP2", "ADMM_S2_L", "ADMM_SWEEP_PF",
+_ENV_KEYS = ("ADMM_PERSIST_GRID", "ADMM_CLUSTER_V", "ADMM_CLUSTER_T", "ADMM_CLUSTER_WARPS", "ADMM_SWEEP_FX", "ADMM_SWEEP2", "ADMM_S2_L", "ADMM_SWEEP_PF",
              "ADMM_SWEEP_CPT", "ADMM_SWEEP_RL")
 
 
