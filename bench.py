@@ -353,7 +353,7 @@ def run_ours(args, W, rank, world, local_rank, dist=None, steps=None, warmup=Non
 def roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms, n_loc=None):
     """Dominant kernel's roofline.  Streaming engines (1, 4): one launch = one ADMM
     iteration, HBM-bound: achieved = algorithmic bytes per iteration / measured time
-    per launch.  On-chip engines (2, 3): one launch = the whole call with the state
+    per launch.  On-chip engines (2, 3, 5): one launch = the whole call with the state
     in shared memory -- latency/sync bound, reported as time per iteration and the
     fp64-pipe utilisation of the committed ncu capture."""
     import numpy as np
@@ -367,7 +367,7 @@ def roofline(args, W, q_loc, engine, kname, iters, sweep_ms, call_ms, n_loc=None
     key = {"configs[3]": f"sweep_q{q_loc}", "configs[1]": "phev", "configs[2]": f"horizon_n{n}",
            "configs[0]": "toy"}.get(W["cfg"], W["cfg"])
     rec = ncu_record(key, kname)
-    if engine in (2, 3):
+    if engine in (2, 3, 5):
         per_it_us = float(np.mean(call_ms)) * 1e3 / float(np.mean(iters))
         return {"bound": "latency/sync", "kernel": kname, "us_per_iteration": per_it_us,
                 "fp64_pipe_pct": rec.get("fp64_pipe_pct") if rec else None,
@@ -464,10 +464,17 @@ def run_quartic(args, W, dev, flush, steps, warmup, e2e):
     hbm = peaks.get("hbm_gbs", 6650.0)
     avg = T / steps
     achieved = 56 * N / avg / 1e9
-    rec = ncu_record("microbench_" + W["family"], "quartic_batch_vec_kernel")
+    # the library samples the batch on the device (quartic_sample_kernel, one CTA) and runs
+    # the per-lane kernel (one branch dominates: family C) or the warp-compacted one (both
+    # branches common: family R) -- both are launched, the other returns at once;
+    # ADMM_QB_WC=0/1 forces one.  Launches per call: 3 (1 forced).
+    forced = os.environ.get("ADMM_QB_WC") in ("0", "1")
+    wc = os.environ.get("ADMM_QB_WC") == "1" if forced else W["family"] == "R"
+    kname = "quartic_batch_wc_kernel" if wc else "quartic_batch_vec_kernel"
+    rec = ncu_record("microbench_" + W["family"], kname)
     res = dict(value=N * steps / T, T=T, iters=[1] * steps, step_ms=ms,
-               clocks=clk.summary(dev.index), gpu_launches=steps, engine="quartic_batch_vec_kernel",
-               roof={"bound": "hbm", "kernel": "quartic_batch_vec_kernel", "achieved": achieved,
+               clocks=clk.summary(dev.index), gpu_launches=steps * (1 if forced else 3), engine=kname,
+               roof={"bound": "hbm", "kernel": kname, "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": rec.get("dram_bytes") if rec else None,
                      "ncu": rec.get("source") if rec else None,

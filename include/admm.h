@@ -85,8 +85,10 @@ typedef enum {
     ADMM_ENGINE_NONE = 0,
     ADMM_ENGINE_STREAM = 1,      /* sweep_kernel: one launch per iteration (graph while loop) */
     ADMM_ENGINE_GRID = 2,        /* persist_kernel: one cooperative launch per call */
-    ADMM_ENGINE_CLUSTER = 3,     /* persist_cluster_kernel: one cluster launch per call */
-    ADMM_ENGINE_STREAM_TMA = 4   /* sweep2_kernel: TMA-fed streaming sweep, one launch per iteration (default for finite boxes) */
+    ADMM_ENGINE_CLUSTER = 3,     /* persist_cluster_kernel: one cluster launch per call (barrier protocol, ADMM_CLUSTER_V=1) */
+    ADMM_ENGINE_STREAM_TMA = 4,  /* sweep2_kernel: TMA-fed streaming sweep, one launch per iteration (default for finite boxes) */
+    ADMM_ENGINE_CLUSTER_MSG = 5  /* persist_cluster2_kernel: one cluster launch per call, message-passing protocol
+                                    (default on-chip engine: PHEV-sized problems) */
 } admm_engine;
 
 /* Multi-GPU partition (one process per GPU; the method is
@@ -268,7 +270,11 @@ void admm_destroy(admm_ctx* ctx);
    (6a) (box_mode PROJECT = clamp of the global minimiser,
    EXACT = minimiser over [lo[e], hi[e]], reading G3).  A >= 0 (A = 0: the
    convex quadratic).  All arrays are DEVICE pointers of length N (caller
-   owned); lo/hi may be NULL (unbounded).  Asynchronous on cuda_stream;
+   owned); lo/hi may be NULL (unbounded).  Asynchronous on cuda_stream: one CTA
+   classifies a strided sample of 4096 quartics and picks, on the device, the
+   one-quartic-per-lane kernel (one branch dominates) or the warp-compacted one
+   (both common: trigonometric-branch quartics are queued per warp so each branch
+   runs with all lanes); results are bit-identical either way.
    ADMM_ERR_INVALID for N < 0, NULL A..D / x or a bad box_mode. */
 admm_status quartic_minimize_batch(const double* A, const double* B, const double* C,
                                    const double* D, const double* lo, const double* hi,

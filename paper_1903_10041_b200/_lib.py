@@ -230,7 +230,7 @@ def admm_get_timing(ctx):
 
 
 ENGINE_NAMES = {0: "none", 1: "sweep_kernel", 2: "persist_kernel", 3: "persist_cluster_kernel",
-                4: "sweep2_kernel"}
+                4: "sweep2_kernel", 5: "persist_cluster2_kernel"}
 
 
 def admm_get_engine(ctx):

@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -443,10 +444,8 @@ __global__ void clear_done_kernel(KArgs a) {
 
 // ---------------------------------------------------------- microbench
 template <int MODE>
-__global__ void __launch_bounds__(256) quartic_batch_vec_kernel(const double* A, const double* B,
-                                                                const double* C, const double* D,
-                                                                const double* lo, const double* hi,
-                                                                double* x, long long N2) {
+__device__ __forceinline__ void qb_vec_body(const double* A, const double* B, const double* C, const double* D,
+                                            const double* lo, const double* hi, double* x, long long N2) {
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N2; t += stride) {
         const double2 a = __ldcs(reinterpret_cast<const double2*>(A) + t);
@@ -461,6 +460,188 @@ __global__ void __launch_bounds__(256) quartic_batch_vec_kernel(const double* A,
         r.y = quartic_boxmin<MODE>(a.y, b.y, c.y, d.y, l.y, h.y);
         __stcs(reinterpret_cast<double2*>(x) + t, r);
     }
+}
+
+// flag (the sampled dispatch): run only when *flag == 0
+template <int MODE>
+__global__ void __launch_bounds__(256) quartic_batch_vec_kernel(const double* A, const double* B,
+                                                                const double* C, const double* D,
+                                                                const double* lo, const double* hi,
+                                                                double* x, long long N2,
+                                                                const int* flag = nullptr) {
+    if (flag && *flag != 0) return;  // the warp-compacted kernel takes this batch
+    qb_vec_body<MODE>(A, B, C, D, lo, hi, x, N2);
+}
+
+// Warp-compacted variant for mixed trigonometric / Cardano batches (PAPER.md:143-161:
+// the two branches of Algorithm 1 have similar cost, so a warp whose lanes split between
+// them pays both).  Each warp streams tiles of 64 quartics (a double2 per lane per
+// stream), normalises and classifies both of each lane's quartics, solves the
+// non-trigonometric ones in place, and appends the trigonometric ones (b, c, d, lo, hi,
+// index) to a per-warp shared-memory queue that is drained 32 at a time with every lane
+// on the trigonometric branch.  No block barrier: a warp's loads still overlap the other
+// warps' fp64 work.  Uniform tiles (all one branch) take the per-lane path.  Every
+// quartic goes through exactly quartic_boxmin's arithmetic: results are bit-identical to
+// quartic_batch_vec_kernel.
+constexpr int QWC_CAP = 96;  // queue slots per warp (<= 31 left + 64 appended per tile)
+
+// quartic_boxmin's normalisation (A != 0) and the cubic's Q, R, Delta
+__device__ __forceinline__ void qwc_norm(double A, double B, double C, double D, double& b, double& c,
+                                         double& d, double& Q, double& R, double& De) {
+    const double ia = 1.0 / A;
+    b = 0.75 * B * ia;
+    c = 0.5 * C * ia;
+    d = 0.25 * D * ia;
+    cubic_qrd(b, c, d, Q, R, De);
+}
+
+template <int MODE>
+__device__ __forceinline__ void qb_wc_body(const double* A, const double* B, const double* C, const double* D,
+                                           const double* lo, const double* hi, double* x, long long N2,
+                                           double (*qf)[5][QWC_CAP], long long (*qi)[QWC_CAP]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    int qn = 0;  // queued trigonometric quartics (warp-uniform)
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long base = ((long long)blockIdx.x * (blockDim.x >> 5) + wid) * 32; base < N2; base += nw * 32) {
+        const long long t = base + lane;
+        const bool in = t < N2;
+        double2 a = make_double2(1.0, 1.0), b = make_double2(0.0, 0.0), c = b, d = b;
+        double2 l = make_double2(-INFINITY, -INFINITY), h = make_double2(INFINITY, INFINITY);
+        if (in) {
+            a = __ldcs(reinterpret_cast<const double2*>(A) + t);
+            b = __ldcs(reinterpret_cast<const double2*>(B) + t);
+            c = __ldcs(reinterpret_cast<const double2*>(C) + t);
+            d = __ldcs(reinterpret_cast<const double2*>(D) + t);
+            if (lo) l = __ldcs(reinterpret_cast<const double2*>(lo) + t);
+            if (hi) h = __ldcs(reinterpret_cast<const double2*>(hi) + t);
+        }
+        const double Av[2] = {a.x, a.y}, Bv[2] = {b.x, b.y}, Cv[2] = {c.x, c.y}, Dv[2] = {d.x, d.y};
+        const double lv[2] = {l.x, l.y}, hv[2] = {h.x, h.y};
+        double bn[2], cn[2], dn[2], Q[2], R[2], De[2];
+        bool tr[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            bn[u] = cn[u] = dn[u] = Q[u] = R[u] = De[u] = 0.0;
+            tr[u] = false;
+            if (Av[u] != 0.0) {
+                qwc_norm(Av[u], Bv[u], Cv[u], Dv[u], bn[u], cn[u], dn[u], Q[u], R[u], De[u]);
+                tr[u] = in && isfinite(De[u]) && !(De[u] > 0.0) && !(Q[u] == 0.0 && R[u] == 0.0);
+            }
+        }
+        const unsigned m0 = __ballot_sync(0xffffffffu, tr[0]), m1 = __ballot_sync(0xffffffffu, tr[1]);
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        if ((m0 | m1) == 0u || (m0 == act && m1 == act)) {  // uniform tile: per-lane path
+            if (in) {
+                double2 r;
+                r.x = Av[0] != 0.0 ? quartic_core_qrd<MODE>(bn[0], cn[0], dn[0], Q[0], R[0], De[0], Cv[0], Dv[0], lv[0], hv[0])
+                                   : clampd(-Dv[0] * rcp_nr(2.0 * Cv[0]), lv[0], hv[0]);
+                r.y = Av[1] != 0.0 ? quartic_core_qrd<MODE>(bn[1], cn[1], dn[1], Q[1], R[1], De[1], Cv[1], Dv[1], lv[1], hv[1])
+                                   : clampd(-Dv[1] * rcp_nr(2.0 * Cv[1]), lv[1], hv[1]);
+                __stcs(reinterpret_cast<double2*>(x) + t, r);
+            }
+            continue;
+        }
+        // append the trigonometric quartics, solve the others in place
+        const int n0 = __popc(m0), n1 = __popc(m1);
+        const int pos[2] = {qn + __popc(m0 & lt), qn + n0 + __popc(m1 & lt)};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (tr[u]) {
+                qf[wid][0][pos[u]] = bn[u];
+                qf[wid][1][pos[u]] = cn[u];
+                qf[wid][2][pos[u]] = dn[u];
+                qf[wid][3][pos[u]] = lv[u];
+                qf[wid][4][pos[u]] = hv[u];
+                qi[wid][pos[u]] = 2 * t + u;
+            } else if (in) {
+                x[2 * t + u] = Av[u] != 0.0 ? quartic_core_qrd<MODE>(bn[u], cn[u], dn[u], Q[u], R[u], De[u], Cv[u], Dv[u], lv[u], hv[u])
+                                            : clampd(-Dv[u] * rcp_nr(2.0 * Cv[u]), lv[u], hv[u]);
+            }
+        }
+        qn += n0 + n1;
+        __syncwarp();
+        while (qn >= 32) {  // one full pass on the trigonometric branch
+            const int k = qn - 32 + lane;
+            const double qb = qf[wid][0][k], qc = qf[wid][1][k], qd = qf[wid][2][k];
+            double QQ, RR, DD;
+            cubic_qrd(qb, qc, qd, QQ, RR, DD);
+            __stcs(x + qi[wid][k], trig_pick<MODE>(qb, qc, qd, QQ, RR, DD, qf[wid][3][k], qf[wid][4][k]));
+            qn -= 32;
+            __syncwarp();
+        }
+    }
+    if (lane < qn) {  // the warp's last partial pass
+        const int k = lane;
+        const double qb = qf[wid][0][k], qc = qf[wid][1][k], qd = qf[wid][2][k];
+        double QQ, RR, DD;
+        cubic_qrd(qb, qc, qd, QQ, RR, DD);
+        __stcs(x + qi[wid][k], trig_pick<MODE>(qb, qc, qd, QQ, RR, DD, qf[wid][3][k], qf[wid][4][k]));
+    }
+}
+
+// flag (the sampled dispatch): run only when *flag == 1
+template <int MODE>
+__global__ void __launch_bounds__(256) quartic_batch_wc_kernel(const double* A, const double* B,
+                                                               const double* C, const double* D,
+                                                               const double* lo, const double* hi,
+                                                               double* x, long long N2,
+                                                               const int* flag = nullptr) {
+    if (flag && *flag != 1) return;  // the per-lane kernel takes this batch
+    __shared__ double qf[8][5][QWC_CAP];  // [warp][b c d lo hi][slot]
+    __shared__ long long qi[8][QWC_CAP];  // [warp][slot] quartic index
+    qb_wc_body<MODE>(A, B, C, D, lo, hi, x, N2, qf, qi);
+}
+
+// Dispatch between the two batch kernels from a strided sample of the batch: one CTA
+// classifies 4096 quartics (every (N/4096)-th) and sets flag = 1 when both branches are
+// common (trigonometric share in [1/64, 63/64]); the per-lane kernel runs when flag == 0
+// and the warp-compacted one when flag == 1 (the other returns at once), so the choice
+// needs no host round trip.
+__device__ int g_qb_flag[64];
+
+__global__ void __launch_bounds__(512) quartic_sample_kernel(const double* A, const double* B, const double* C,
+                                                             const double* D, long long N, int* flag) {
+    // 512 threads x 8 samples, every load issued before any arithmetic (one memory round trip)
+    constexpr int PER = 8, NS = 512 * PER;
+    __shared__ int cnt[2];
+    if (threadIdx.x < 2) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const long long step = N >= NS ? N / NS : 1;
+    double a[PER], b[PER], c[PER], d[PER];
+    bool ok[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const long long i = (long long)(u * 512 + threadIdx.x) * step;
+        ok[u] = i < N;
+        a[u] = ok[u] ? __ldg(A + i) : 0.0;
+        b[u] = ok[u] ? __ldg(B + i) : 0.0;
+        c[u] = ok[u] ? __ldg(C + i) : 0.0;
+        d[u] = ok[u] ? __ldg(D + i) : 0.0;
+    }
+    int nt = 0, nall = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        if (!ok[u]) continue;
+        ++nall;
+        if (a[u] != 0.0) {
+            double bn, cn, dn, Q, R, De;
+            const double ia = 1.0 / a[u];
+            bn = 0.75 * b[u] * ia;
+            cn = 0.5 * c[u] * ia;
+            dn = 0.25 * d[u] * ia;
+            cubic_qrd(bn, cn, dn, Q, R, De);
+            nt += (isfinite(De) && !(De > 0.0) && !(Q == 0.0 && R == 0.0)) ? 1 : 0;
+        }
+    }
+    nt = __reduce_add_sync(0xffffffffu, nt);
+    nall = __reduce_add_sync(0xffffffffu, nall);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&cnt[0], nt);
+        atomicAdd(&cnt[1], nall);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = (64 * cnt[0] >= cnt[1] && 64 * cnt[0] <= 63 * cnt[1]) ? 1 : 0;
 }
 
 template <int MODE>
@@ -1129,7 +1310,7 @@ C2Plan plan_cluster2(admm_ctx* ctx, const void* fn) {
             const long long G = q * T;
             const long long k = std::max((TC0 + b0 - 1) / b0, (TC + b1 - 1) / b1);  // cells per thread
             // CTAs per SM: register file (128 regs x 32 lanes per warp) and shared memory
-            const long long by_regs = 64 / NW, by_smem = (228 * 1024) / (long long)(oc2_smem(m, TCM, T, NW) + 1024);
+            const long long by_regs = 65536LL / (32LL * NW * OC2_REGS), by_smem = (228 * 1024) / (long long)(oc2_smem(m, TCM, T, NW) + 1024);
             const long long per_sm_cap = std::max(1LL, std::min(by_regs, by_smem));
             const long long cps = (G + sms - 1) / sms;
             if (cps > per_sm_cap) continue;
@@ -1261,7 +1442,7 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
             return fail(ctx, ADMM_ERR_INVALID,
                         "horizon blocks need the TMA sweep: finite boxes and m <= 4");
     }
-    ctx->last_engine = (cpl.ok || c2pl.ok) ? ADMM_ENGINE_CLUSTER
+    ctx->last_engine = c2pl.ok ? ADMM_ENGINE_CLUSTER_MSG : cpl.ok ? ADMM_ENGINE_CLUSTER
                               : (pl.ok ? ADMM_ENGINE_GRID
                                        : (ctx->use_tma ? ADMM_ENGINE_STREAM_TMA : ADMM_ENGINE_STREAM));
     upload_params(ctx, iter_limit, stop_on_conv);
@@ -1946,10 +2127,34 @@ admm_status quartic_minimize_batch(const double* A, const double* B, const doubl
     if (vec) {
         const long long N2 = N / 2;
         const int grid = (int)std::min<long long>((N2 + bs - 1) / bs, (long long)sms * 8);
-        if (box_mode == 1)
-            quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
-        else
-            quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+        // default: sample the batch on the device and run the per-lane or the warp-compacted
+        // kernel; ADMM_QB_WC=0 / 1 forces one of them (experiments)
+        const char* wc = getenv("ADMM_QB_WC");
+        if (wc && (wc[0] == '0' || wc[0] == '1')) {
+            if (wc[0] == '1') {
+                if (box_mode == 1) quartic_batch_wc_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+                else quartic_batch_wc_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+            } else if (box_mode == 1) {
+                quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+            } else {
+                quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+            }
+        } else {
+            // the decision lives in one of 64 device words used round-robin (calls in flight
+            // on several streams at once each get their own word)
+            static std::atomic<unsigned> next_slot{0};
+            int* flags = nullptr;
+            if (cudaGetSymbolAddress((void**)&flags, g_qb_flag) != cudaSuccess) return ADMM_ERR_CUDA;
+            int* flag = flags + (next_slot.fetch_add(1) % 64);
+            quartic_sample_kernel<<<1, 512, 0, st>>>(A, B, C, D, N, flag);
+            if (box_mode == 1) {
+                quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+                quartic_batch_wc_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+            } else {
+                quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+                quartic_batch_wc_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+            }
+        }
     } else {
         const int grid = (int)std::min<long long>((N + bs - 1) / bs, (long long)sms * 8);
         if (box_mode == 1)

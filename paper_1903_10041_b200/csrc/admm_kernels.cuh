@@ -613,16 +613,21 @@ __device__ inline void finalize_global(const KArgs& a, const double* agg, int wo
     const DParams& P = *a.prm;
     const int m = a.m;
     // (6c) PAPER.md:436 with the mean (reading G1): x1 = (1/q) sum_j (x_1 - nu)
+    // loops over MAXM with a predicate (not over m): constant indices keep x1n and t in
+    // registers (no local memory in the sweep kernels that inline this)
     double x1n[MAXM];
-    for (int i = 0; i < m; ++i) {
+#pragma unroll
+    for (int i = 0; i < MAXM; ++i) {
         double s = 0.0;
-        for (int r = 0; r < world; ++r) s += agg[r * XB + i];
+        if (i < m)
+            for (int r = 0; r < world; ++r) s += agg[r * XB + i];
         x1n[i] = s / (double)a.q_total;
     }
     for (int l = 0; l < 4; ++l) {
         cout.rho[l] = cin.rho[l];
         cout.f[l] = 1.0;
     }
+#pragma unroll
     for (int i = 0; i < MAXM; ++i) cout.x1[i] = i < m ? x1n[i] : 0.0;
     cout.r = cin.r;
     cout.sigma = cin.sigma;
@@ -638,9 +643,10 @@ __device__ inline void finalize_global(const KArgs& a, const double* agg, int wo
             t[0] = fmax(t[0], g[3 * MAXM + 0]);
             t[1] = fmax(t[1], g[3 * MAXM + 1]);
             t[2] = fmax(t[2], g[3 * MAXM + 2]);
-            for (int i = 0; i < m; ++i) {
+#pragma unroll
+            for (int i = 0; i < MAXM; ++i) {
                 // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
-                t[3] = fmax(t[3], fmax(g[MAXM + i] - x1n[i], x1n[i] - g[2 * MAXM + i]));
+                if (i < m) t[3] = fmax(t[3], fmax(g[MAXM + i] - x1n[i], x1n[i] - g[2 * MAXM + i]));
             }
             t[4] = fmax(t[4], g[3 * MAXM + 3]);
             t[5] = fmax(t[5], g[3 * MAXM + 4]);

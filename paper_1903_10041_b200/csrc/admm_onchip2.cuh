@@ -41,6 +41,7 @@
 namespace admm_dev {
 
 constexpr int OC2_MAX_W = 16;  // warps per CTA (tile 0: NW-1 bulk warps + the consensus warp)
+constexpr int OC2_REGS = 128;  // registers per thread (4 warps of 128 fill one SM sub-partition's 16K)
 constexpr int OC2_MAX_T = 16;  // CTAs per cluster
 constexpr int OC2_BUFS = 4;    // rotating LL buffers: (6c) contributions, check words
 constexpr int OC2_CHKV = 6;    // per-row check values: r1 r2 r3 s1 s2 s3

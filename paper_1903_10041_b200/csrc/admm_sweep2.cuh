@@ -633,7 +633,9 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
     if (!s_last) return;
     __threadfence();
     // ---- last CTA: reduce the G CTA partials; lane = slot, warp w takes CTAs w, w + NW,
-    // ... with eight independent accumulators (fixed assignment => deterministic)
+    // ... 32 loads in flight per lane per pass (the pass count, not the bytes, sets this
+    // tail's latency: G = 592 at q = 1e3 takes 5 L2 round trips instead of 19), folded
+    // into eight accumulators in a fixed order (fixed assignment => deterministic)
     {
         __shared__ double wred[S2_NW][XB];
         const int sl = lane;
@@ -643,16 +645,16 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
         double vv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) vv[u] = ident;
-        for (int g0 = wid; g0 < s.G; g0 += 8 * S2_NW) {
-            double t[8];
+        for (int g0 = wid; g0 < s.G; g0 += 32 * S2_NW) {
+            double t[32];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 32; ++u) {
                 const int g = g0 + u * S2_NW;
                 t[u] = g < s.G ? __ldcg(a.cta_part + (size_t)g * XB + sl) : ident;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                vv[u] = is_sum ? vv[u] + t[u] : (is_min ? fmin(vv[u], t[u]) : fmax(vv[u], t[u]));
+            for (int u = 0; u < 32; ++u)
+                vv[u & 7] = is_sum ? vv[u & 7] + t[u] : (is_min ? fmin(vv[u & 7], t[u]) : fmax(vv[u & 7], t[u]));
         }
         double vr = vv[0];
 #pragma unroll

@@ -138,7 +138,7 @@ def test_gpu_fp32_coefficients_phev_q50(iters, engine):
     o = oracle.Oracle(Q, prm)
     io, ho = o.run(iters)
     Sg, sol, hg, eng = _gpu(P, prm, iters, engine)
-    assert eng == {"stream": 4, "stream_legacy": 1, "stream_fx": 1, "cluster": 3, "grid": 2}[engine]
+    assert eng == {"stream": 4, "stream_legacy": 1, "stream_fx": 1, "cluster": 5, "grid": 2}[engine]
     compare_states(Q, o.state(), Sg)
     check_hist(ho, hg, Q, o.state())
     assert abs(sol["objective"] - io["objective"]) <= 1e-9 * abs(io["objective"])

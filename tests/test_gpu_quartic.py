@@ -107,3 +107,31 @@ def test_microbench_full_size_sampled(family):
     Jg, Jo = _J(*s[:4], s[6]), _J(*s[:4], xo)
     assert np.all(Jg <= Jo + 1e-12 * (1 + _Jscale(*s[:4], xo)))
     assert np.all(s[6] >= s[4]) and np.all(s[6] <= s[5])
+
+
+@pytest.mark.parametrize("fam", ["R", "C", "phev", "spread", "quadratic"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_batch_kernels_bit_identical(fam, mode):
+    """The sampled dispatch (default), the one-quartic-per-lane kernel (ADMM_QB_WC=0)
+    and the warp-compacted kernel (ADMM_QB_WC=1, trigonometric quartics queued per warp)
+    run Algorithm 1 with the same arithmetic: bitwise-identical minimisers, including a
+    ragged tail (N odd is the scalar kernel; N = 2 mod 64 leaves a partial warp tile and
+    a partial queue pass)."""
+    import os
+
+    F, rng = _families(2 * 100_001, 47)
+    A, B, C, D = F[fam]
+    sc = 1e5 if fam == "phev" else 5.0
+    lo = -sc * rng.uniform(0, 1, A.size)
+    hi = sc * rng.uniform(0, 1, A.size)
+    outs = []
+    for env in (None, "0", "1"):
+        if env is None:
+            os.environ.pop("ADMM_QB_WC", None)
+        else:
+            os.environ["ADMM_QB_WC"] = env
+        try:
+            outs.append(_gpu(A, B, C, D, lo, hi, mode))
+        finally:
+            os.environ.pop("ADMM_QB_WC", None)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
