@@ -111,7 +111,7 @@ __device__ __forceinline__ void ll_consensus(const unsigned long long* buf, long
 #pragma unroll
         for (int i = 0; i < M; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
 #pragma unroll
-    for (int i = 0; i < M; ++i) x1[i] = s[i] / qtot;
+    for (int i = 0; i < M; ++i) x1[i] = s[i] * (1.0 / qtot);
 }
 
 // ------------------------------------------------------- cluster messaging
@@ -287,7 +287,7 @@ __device__ __noinline__ void oc2_check(const C2Args& p, double* hist, int hist_c
         for (int i = 0; i < M; ++i) xs[i] += __shfl_xor_sync(0xffffffffu, xs[i], o);
     double x1v[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x1v[i] = xs[i] / qtot;
+    for (int i = 0; i < M; ++i) x1v[i] = xs[i] * (1.0 / qtot);
     // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
     double t3 = 0.0;
 #pragma unroll
@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
             dgn[i] = INFINITY;
         }
         double my_r1 = 0.0, my_s3 = 0.0;
+        bool sent = false;  // the consensus warp sends its partial early (non-check iterations)
         if (!cons_warp) {
             // ---- bulk cells c = tid (mod nbt), except the consensus cell k = 0.
             // Pairs (cc, cc + nbt) go through the interleaved two-cell chain.
@@ -671,10 +672,27 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
                     c_x0 = x0[i];
                     c_pub = x0[i] - cnu[i];
                 }
+            if (lane < M && (!single || is_check))  // q = 1: only the residual check reads it
+                ll_store(p.pub + 2 * ((size_t)(u & 3) * M * qq + (size_t)lane * qq + j), c_pub, (unsigned)(u + 1));
+            if (!is_check) {
+                // the row update waits on this partial: send it before the cell's bookkeeping
+                unsigned long long w0[MS];
+#pragma unroll
+                for (int i = 0; i < MS; ++i) {
+                    long long f = 0;
+                    if (i < M && !((a.gfree >> i) & 1u))
+                        f = __double2ll_rn(fma(cb2[i], x0[i], cb1[i]) * x0[i] * p.fx_scale[i]);
+                    w0[i] = (unsigned long long)__shfl_sync(0xffffffffu, f, 0);
+                }
+                if (lane < T) {
+                    const unsigned rb = mapa_u32(bar0 + 8 * par, rank_l);
+                    const unsigned rs = mapa_u32(my_rs + par * rs_par, rank_l);
+#pragma unroll
+                    for (int i = 0; i < MS; i += 2) st_async2(rs + 8 * i, w0[i], w0[i + 1], rb);
+                }
+                sent = true;
+            }
             if (lane < M) {
-                if (!single || is_check)  // q = 1: only the residual check reads it
-                    ll_store(p.pub + 2 * ((size_t)(u & 3) * M * qq + (size_t)lane * qq + j), c_pub,
-                             (unsigned)(u + 1));
                 s_con[0][lane] = c_nu;
                 s_con[1][lane] = c_x1;
                 s_con[2][lane] = c_x0;
@@ -706,7 +724,7 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
         PHASE2(2)
 
         // ---- every warp: exact fixed-point warp sums (+ check keys) to every mate (st.async)
-        {
+        if (!sent) {
             unsigned long long ws[MS];
 #pragma unroll
             for (int i = 0; i < MS; ++i) ws[i] = i < M ? warp_sum_u64((unsigned long long)fx[i]) : 0ull;
