@@ -534,3 +534,45 @@ def test_streaming_engine_bitwise_deterministic(env):
     for k in STATE_KEYS:
         assert np.array_equal(S0[k], S1[k]), k
     assert np.array_equal(h0, h1)
+
+
+@pytest.mark.parametrize("env", [{}, {"ADMM_CLUSTER_T": "3", "ADMM_CLUSTER_WARPS": "2"},
+                                 {"ADMM_CLUSTER_V": "1"}], ids=["msg", "msg_t3w2", "barrier"])
+def test_cluster_engine_bitwise_deterministic_and_resumable(env):
+    """The on-chip engines' cross-CTA protocols (st.async row slots + mbarriers and
+    epoch-tagged L2 words; DSMEM atomics + cluster barriers) must not race: three runs of
+    PHEV q=50 for 300 iterations (30 checks, rho adaptation) agree bit for bit in every
+    state array and in the history, and splitting the run into calls of 137 + 163
+    iterations (a call boundary inside a check period: (6h) and the epochs restart)
+    gives the same bits."""
+    import os
+
+    L = _lib()
+    P = synth.phev_problem(1000, 50)
+    prm = oracle.default_params(r_bar=1e-6 * P["c"][1])
+
+    def run(split):
+        for k in _ENV_KEYS:
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        try:
+            s = L.AdmmSolver(2, 1000, 50, rho=prm["rho0"], r_bar=prm["r_bar"], exec_mode=2)
+            s.set_problem(P)
+            for n in split:
+                s.iterate(n)
+            out = (s.state(), s.history(), L._lib.ENGINE_NAMES.get(s.engine()[0]))
+            s.close()
+            return out
+        finally:
+            for k in _ENV_KEYS:
+                os.environ.pop(k, None)
+
+    runs = [run([300]), run([300]), run([300]), run([137, 163])]
+    want = "persist_cluster_kernel" if env.get("ADMM_CLUSTER_V") == "1" else "persist_cluster2_kernel"
+    for S, h, e in runs:
+        assert e == want
+    S0, h0, _ = runs[0]
+    for S, h, _ in runs[1:]:
+        for k in STATE_KEYS:
+            assert np.array_equal(np.asarray(S0[k]), np.asarray(S[k])), k
+        assert np.array_equal(h0, h)
