@@ -199,29 +199,36 @@ __host__ __device__ inline size_t oc2_msg_bytes(int M, int T, int nw) {
     return (size_t)2 * T * nw * (((M + 1) & ~1) + 2 * M + 2) * 8;
 }
 
-// Residual check of iteration it (row warp of every CTA): publish this row's six maxima
-// (tile 0, LL words) and count the arrival, wait until all 2q arrivals of check c are in
-// (one lane polls the relaxed counter), read every row's words and this iteration's (6c)
-// contributions (LL: a word not yet visible is re-read), reduce them in a fixed order, take
-// the termination / rho decision (readings G10-G12; the
-// arithmetic of check_decide), rescale lam / p (reading G11) and hand rho, f, x1, r, sigma
-// and the flags to the CTA through shared memory.  x1 is summed in the order of
-// ll_consensus (lane-strided j, then the butterfly): the bits the consensus warps compute.
+// Residual check of iteration it (row warp of every CTA).  Tile 0 of each row publishes the
+// row's six maxima (LL words) and counts the arrival, waits until all 2q arrivals of check c
+// are in (one lane polls the relaxed counter), reads every row's words and this iteration's
+// (6c) contributions (LL: a word not yet visible is re-read), reduces them in a fixed order
+// and takes the termination / rho decision (readings G10-G12;
+// the arithmetic of check_decide); it then forwards the decision (16 doubles) to the other
+// CTAs of its row with st.async on their decision mbarrier, so only q warps read L2, not q T.
+// Every CTA rescales lam / p (reading G11) and hands rho, f, x1, r, sigma and the flags to
+// its cells through shared memory.  x1 is summed in the order of ll_consensus (lane-strided
+// j, then the butterfly): the bits the consensus warps compute.
+constexpr int OC2_DEC = 16;  // decision record: rho_new[4] f[4] r sigma conv dir x1[M <= 4]
+
 template <int M>
-__device__ __noinline__ void oc2_check(const C2Args& p, double* hist, int hist_cap, double nd, int tile,
+__device__ __noinline__ void oc2_check(const C2Args& p, double* hist, int hist_cap, double nd, int tile, int T,
                                        long long j, long long qq, double qtot, long long u, long long it,
                                        unsigned nchk, double r2, double r3, double s1, double s2,
                                        unsigned long long kr1, unsigned long long ks3, double* s_rho,
                                        double* s_f, double* s_R, double* s_t, int* s_flag, int* s_chk,
-                                       double* s_kap, double* s_x1, double* r_lam, double* r_p) {
+                                       double* s_kap, double* s_x1, double* r_lam, double* r_p,
+                                       double* s_dec, unsigned dbar0) {
     const int lane = threadIdx.x & 31;
     const DParams& P = p.prm;
 #ifdef ADMM_PHASE_PROF
     unsigned long long c_last = clock64();
 #endif
     const unsigned cep = nchk + 1, pep = (unsigned)(u + 1);
-    unsigned long long* cbuf = p.chkv + 2 * (size_t)(nchk & (OC2_BUFS - 1)) * qq * OC2_CHKV;
+    const unsigned db = nchk & 1u;                 // decision buffer / mbarrier of this check
+    double dec[OC2_DEC];
     if (tile == 0) {
+        unsigned long long* cbuf = p.chkv + 2 * (size_t)(nchk & (OC2_BUFS - 1)) * qq * OC2_CHKV;
         // row maxima over the sources (lanes i < M hold r2, r3, s1, s2 >= 0, or NaN)
         const unsigned long long k2 = warp_max_key(nbits(r2)), k3 = warp_max_key(nbits(r3));
         const unsigned long long k4 = warp_max_key(nbits(s1)), k5 = warp_max_key(nbits(s2));
@@ -232,144 +239,146 @@ __device__ __noinline__ void oc2_check(const C2Args& p, double* hist, int hist_c
         }
         __syncwarp();
         if (lane == 0) gred_add_relaxed(p.cnt, 1u);
-    }
-    CPHASE(0)
-    const unsigned target = 2u * (unsigned)qq * (nchk + 1);
-    if (lane == 0)
-        while (ld_relaxed_u32(p.cnt) < target) __nanosleep(20);
-    __syncwarp();
-    CPHASE(1)
-    // rows j = lane + 32 b: six maxima, x_1, (6c) contribution (LL words, re-read until current)
-    const unsigned long long* xbuf = p.chkx + 2 * (size_t)(nchk & (OC2_BUFS - 1)) * M * qq;
-    const unsigned long long* pbuf = p.pub + 2 * (size_t)(u & (OC2_BUFS - 1)) * M * qq;
-    unsigned long long km[OC2_CHKV + 2 * M];  // maxima keys: r1..s3 bits, okey(x_1), okey(-x_1)
-    double xs[M];
+        CPHASE(0)
+        const unsigned target = 2u * (unsigned)qq * (nchk + 1);
+        if (lane == 0)
+            while (ld_relaxed_u32(p.cnt) < target) __nanosleep(20);
+        __syncwarp();
+        CPHASE(1)
+        // rows j = lane + 32 b: six maxima, x_1, (6c) contribution (LL words, re-read until current)
+        const unsigned long long* xbuf = p.chkx + 2 * (size_t)(nchk & (OC2_BUFS - 1)) * M * qq;
+        const unsigned long long* pbuf = p.pub + 2 * (size_t)(u & (OC2_BUFS - 1)) * M * qq;
+        unsigned long long km[OC2_CHKV + 2 * M];  // maxima keys: r1..s3 bits, okey(x_1), okey(-x_1)
+        double xs[M];
 #pragma unroll
-    for (int s = 0; s < OC2_CHKV + 2 * M; ++s) km[s] = 0ull;
+        for (int s = 0; s < OC2_CHKV + 2 * M; ++s) km[s] = 0ull;
 #pragma unroll
-    for (int i = 0; i < M; ++i) xs[i] = 0.0;
-    for (long long jb = 0; jb < qq; jb += 32) {
-        const long long jj = jb + lane;
-        double v[OC2_CHKV], xv[M], pv[M];
-        for (;;) {
-            bool ok = true;
+        for (int i = 0; i < M; ++i) xs[i] = 0.0;
+        for (long long jb = 0; jb < qq; jb += 32) {
+            const long long jj = jb + lane;
+            double v[OC2_CHKV], xv[M], pv[M];
+            for (;;) {
+                bool ok = true;
+                if (jj < qq) {
+#pragma unroll
+                    for (int s = 0; s < OC2_CHKV; ++s)
+                        ok = ll_load(cbuf + 2 * ((size_t)jj * OC2_CHKV + s), cep, &v[s]) && ok;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        ok = ll_load(xbuf + 2 * ((size_t)i * qq + jj), cep, &xv[i]) && ok;
+                        ok = ll_load(pbuf + 2 * ((size_t)i * qq + jj), pep, &pv[i]) && ok;
+                    }
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+            }
             if (jj < qq) {
 #pragma unroll
-                for (int s = 0; s < OC2_CHKV; ++s) ok = ll_load(cbuf + 2 * ((size_t)jj * OC2_CHKV + s), cep, &v[s]) && ok;
+                for (int s = 0; s < OC2_CHKV; ++s) km[s] = max(km[s], nbits(v[s]));
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    ok = ll_load(xbuf + 2 * ((size_t)i * qq + jj), cep, &xv[i]) && ok;
-                    ok = ll_load(pbuf + 2 * ((size_t)i * qq + jj), pep, &pv[i]) && ok;
+                    km[OC2_CHKV + i] = max(km[OC2_CHKV + i], okey(xv[i]));
+                    km[OC2_CHKV + M + i] = max(km[OC2_CHKV + M + i], okey(-xv[i]));
+                    xs[i] += pv[i];
                 }
+            } else {
+#pragma unroll
+                for (int i = 0; i < M; ++i) xs[i] += 0.0;
             }
-            if (__all_sync(0xffffffffu, ok)) break;
         }
-        if (jj < qq) {
+        CPHASE(2)
 #pragma unroll
-            for (int s = 0; s < OC2_CHKV; ++s) km[s] = max(km[s], nbits(v[s]));
+        for (int s = 0; s < OC2_CHKV + 2 * M; ++s) km[s] = warp_max_key(km[s]);
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                km[OC2_CHKV + i] = max(km[OC2_CHKV + i], okey(xv[i]));
-                km[OC2_CHKV + M + i] = max(km[OC2_CHKV + M + i], okey(-xv[i]));
-                xs[i] += pv[i];
-            }
-        } else {
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-            for (int i = 0; i < M; ++i) xs[i] += 0.0;
+            for (int i = 0; i < M; ++i) xs[i] += __shfl_xor_sync(0xffffffffu, xs[i], o);
+        double x1v[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) x1v[i] = xs[i] * (1.0 / qtot);
+        // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
+        double t3 = 0.0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const double xmx = okey_inv(km[OC2_CHKV + i]);
+            const double xmn = -okey_inv(km[OC2_CHKV + M + i]);
+            t3 = fmax(t3, fmax(xmx - x1v[i], x1v[i] - xmn));
         }
-    }
-    CPHASE(2)
-#pragma unroll
-    for (int s = 0; s < OC2_CHKV + 2 * M; ++s) km[s] = warp_max_key(km[s]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < M; ++i) xs[i] += __shfl_xor_sync(0xffffffffu, xs[i], o);
-    double x1v[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) x1v[i] = xs[i] * (1.0 / qtot);
-    // max_j |x_1^{(i,j)} - x1| = max(max_j x_1 - x1, x1 - min_j x_1) exactly
-    double t3 = 0.0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        const double xmx = okey_inv(km[OC2_CHKV + i]);
-        const double xmn = -okey_inv(km[OC2_CHKV + M + i]);
-        t3 = fmax(t3, fmax(xmx - x1v[i], x1v[i] - xmn));
-    }
-    const double tt[7] = {nbits_inv(km[0]), nbits_inv(km[1]), nbits_inv(km[2]), t3,
-                          nbits_inv(km[3]), nbits_inv(km[4]), nbits_inv(km[5])};
-    // check_decide (admm_kernels.cuh) with the thresholds prepared on the host
-    const double rho0 = s_rho[0], rho1 = s_rho[1], rho2 = s_rho[2], rho3 = s_rho[3];
-    const double sg1 = rho0 * tt[4], sg2 = rho1 * tt[5], sg3 = rho2 * tt[6];
-    const double r = fmax(fmax(tt[0], tt[1]), fmax(tt[2], tt[3]));
-    const double sg = fmax(sg1, fmax(sg2, sg3));
-    const int conv = (r < P.r_bar) && (sg < P.sigma_bar);
-    int dir = 0;
-    if (!conv && P.adapt) {
-        const double ratio = (sg > 0.0) ? r / sg : INFINITY;  // reading G12
-        if (ratio > p.thr_hi) dir = 1;
-        else if (ratio < p.thr_lo) dir = -1;
-    }
-    const double rho[4] = {rho0, rho1, rho2, rho3};
-    CPHASE(3)
-    const int chk = *s_chk;
-    if (dir == 0) {
-        if (blockIdx.x == 0 && lane == 0 && hist && hist_cap > 0) {
-            const double s123[3] = {sg1, sg2, sg3};
-            write_hist(hist + (size_t)(chk % hist_cap) * HCOLS, it + 1, r, sg, rho, tt, s123, conv, 1.0);
+        const double tt[7] = {nbits_inv(km[0]), nbits_inv(km[1]), nbits_inv(km[2]), t3,
+                              nbits_inv(km[3]), nbits_inv(km[4]), nbits_inv(km[5])};
+        // check_decide (admm_kernels.cuh) with the thresholds prepared on the host
+        const double rho[4] = {s_rho[0], s_rho[1], s_rho[2], s_rho[3]};
+        const double sg1 = rho[0] * tt[4], sg2 = rho[1] * tt[5], sg3 = rho[2] * tt[6];
+        const double r = fmax(fmax(tt[0], tt[1]), fmax(tt[2], tt[3]));
+        const double sg = fmax(sg1, fmax(sg2, sg3));
+        const int conv = (r < P.r_bar) && (sg < P.sigma_bar);
+        int dir = 0;
+        if (!conv && P.adapt) {
+            const double ratio = (sg > 0.0) ? r / sg : INFINITY;  // reading G12
+            if (ratio > p.thr_hi) dir = 1;
+            else if (ratio < p.thr_lo) dir = -1;
         }
-        __syncwarp();
-        if (lane < M) {
-#pragma unroll
-            for (int i = 0; i < M; ++i)
-                if (lane == i) s_x1[i] = x1v[i];
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int l = 0; l < 4; ++l) s_f[l] = 1.0;
-            s_t[0] = r;
-            s_t[1] = sg;
-            s_flag[0] = conv;
-            s_flag[1] = s_flag[1] | ((!isfinite(r) || !isfinite(sg)) ? 1 : 0);
-            *s_chk = chk + 1;
-        }
-    } else {
-        double rn[4], fl[4];
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            rn[l] = dir > 0 ? rho[l] * P.tau : rho[l] / P.tau;
-            fl[l] = P.rescale ? rho[l] / rn[l] : 1.0;
+            dec[l] = dir > 0 ? rho[l] * P.tau : dir < 0 ? rho[l] / P.tau : rho[l];
+            dec[4 + l] = (dir != 0 && P.rescale) ? rho[l] / dec[l] : 1.0;
         }
-        const double fac = dir > 0 ? P.tau : 1.0 / P.tau;
+        dec[8] = r;
+        dec[9] = sg;
+        dec[10] = conv;
+        dec[11] = dir;
+#pragma unroll
+        for (int i = 0; i < OC2_DEC - 12; ++i) dec[12 + i] = i < M ? x1v[i < M ? i : 0] : 0.0;
         if (blockIdx.x == 0 && lane == 0 && hist && hist_cap > 0) {
             const double s123[3] = {sg1, sg2, sg3};
-            write_hist(hist + (size_t)(chk % hist_cap) * HCOLS, it + 1, r, sg, rho, tt, s123, conv, fac);
+            const double fac = dir > 0 ? P.tau : dir < 0 ? 1.0 / P.tau : 1.0;
+            write_hist(hist + (size_t)(*s_chk % hist_cap) * HCOLS, it + 1, r, sg, rho, tt, s123, conv, fac);
+        }
+        // forward the decision to the row's other CTAs (lane t -> CTA t)
+        if (lane >= 1 && lane < T) {
+            const unsigned rb = mapa_u32(dbar0 + 8 * db, (unsigned)lane);
+            const unsigned rd = mapa_u32(smem_u32(s_dec + db * OC2_DEC), (unsigned)lane);
+#pragma unroll
+            for (int s = 0; s < OC2_DEC; s += 2) st_async2(rd + 8 * s, nbits(dec[s]), nbits(dec[s + 1]), rb);
+        }
+    } else {
+        // the decision of this row's tile 0
+        if (lane == 0) {
+            mbar_expect(dbar0 + 8 * db, (unsigned)(OC2_DEC * 8));
+            mbar_wait_cluster(dbar0 + 8 * db, (nchk >> 1) & 1u);
         }
         __syncwarp();
-        if (lane < M) {  // dual rescale (reading G11): lam<->rho1, p<->rho2
-            *r_lam *= fl[0];
-            *r_p *= fl[1];
 #pragma unroll
-            for (int i = 0; i < M; ++i)
-                if (lane == i) s_x1[i] = x1v[i];
-        }
-        if (lane == 0) {
+        for (int s = 0; s < OC2_DEC; ++s) dec[s] = ((volatile double*)s_dec)[db * OC2_DEC + s];
+    }
+    CPHASE(3)
+    const int conv = dec[10] != 0.0, dir = (int)dec[11];
+    const double r = dec[8], sg = dec[9];
+    __syncwarp();
+    if (lane < M) {  // dual rescale (reading G11): lam<->rho1, p<->rho2 (factors 1 without a change)
+        *r_lam *= dec[4];
+        *r_p *= dec[5];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                s_rho[l] = rn[l];
-                s_f[l] = fl[l];
-            }
-            s_R[0] = rn[0];
-            s_R[1] = rn[2];
-            s_R[2] = rn[3];
-            s_R[3] = 1.0 / rn[0];
-            s_t[0] = r;
-            s_t[1] = sg;
-            s_flag[0] = conv;
-            s_flag[1] = s_flag[1] | ((!isfinite(r) || !isfinite(sg)) ? 1 : 0);
-            *s_chk = chk + 1;
-            *s_kap = rn[1] / (rn[0] + nd * rn[1]);
+        for (int i = 0; i < M; ++i)
+            if (lane == i) s_x1[i] = dec[12 + i];
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            s_rho[l] = dec[l];
+            s_f[l] = dec[4 + l];
         }
+        if (dir != 0) {
+            s_R[0] = dec[0];
+            s_R[1] = dec[2];
+            s_R[2] = dec[3];
+            s_R[3] = 1.0 / dec[0];
+            *s_kap = dec[1] / (dec[0] + nd * dec[1]);
+        }
+        s_t[0] = r;
+        s_t[1] = sg;
+        s_flag[0] = conv;
+        s_flag[1] = s_flag[1] | ((!isfinite(r) || !isfinite(sg)) ? 1 : 0);
+        *s_chk = *s_chk + 1;
     }
     __syncwarp();
     CPHASE(4)
@@ -402,6 +411,8 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
     unsigned long long* s_ck = s_rs + (size_t)2 * NS * MS;
 
     __shared__ __align__(8) unsigned long long s_mbar[2];
+    __shared__ __align__(8) unsigned long long s_dbar[2];  // check decisions from tile 0 (by check parity)
+    __shared__ __align__(16) double s_dec[2][OC2_DEC];
     __shared__ double s_zl[M], s_x1[M], s_R[4], s_rho[4], s_f[4], s_t[2], s_kap;
     __shared__ int s_flag[2], s_chk;  // conv, err; checks done (all calls)
     // role state kept in shared memory, not registers (the cell code needs them):
@@ -490,6 +501,8 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
         s_chk = cin.checks;
         mbar_init(smem_u32(&s_mbar[0]), 1);
         mbar_init(smem_u32(&s_mbar[1]), 1);
+        mbar_init(smem_u32(&s_dbar[0]), 1);
+        mbar_init(smem_u32(&s_dbar[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     int l_done = 0;
@@ -820,8 +833,9 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
             }
             PHASE2(5)
             if (is_check)
-                oc2_check<M>(p, a.hist, a.hist_cap, nd, tile, j, qq, qtot, u, it, nchk, r2, r3, s1, s2, kr1, ks3,
-                             s_rho, s_f, s_R, s_t, s_flag, &s_chk, &s_kap, s_x1, &r_lam, &r_p);
+                oc2_check<M>(p, a.hist, a.hist_cap, nd, tile, T, j, qq, qtot, u, it, nchk, r2, r3, s1, s2, kr1, ks3,
+                             s_rho, s_f, s_R, s_t, s_flag, &s_chk, &s_kap, s_x1, &r_lam, &r_p, &s_dec[0][0],
+                             smem_u32(&s_dbar[0]));
             if (lane < M) {
                 s_row[0][lane] = r_lam;
                 s_row[1][lane] = r_p;
