@@ -1,5 +1,8 @@
-"""Per-phase cycles of the cluster kernel (dev build with -DADMM_PHASE_PROF, ADMM_SO=...)."""
+"""Per-phase cycles of the barrier cluster kernel (persist_cluster_kernel, selected with
+ADMM_CLUSTER_V=1; dev build with -DADMM_PHASE_PROF, ADMM_SO=...).  The message-passing engine
+has its own probe, tools/probe_phase2.py."""
 import ctypes as C, os, sys
+os.environ["ADMM_CLUSTER_V"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch  # noqa: F401  (load torch's NCCL first)
