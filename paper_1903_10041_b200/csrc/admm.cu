@@ -495,10 +495,18 @@ __device__ __forceinline__ void qwc_norm(double A, double B, double C, double D,
     cubic_qrd(b, c, d, Q, R, De);
 }
 
+constexpr int QWC_NW = 8;  // warps per CTA of the warp-compacted kernel
+
+// flag (the sampled dispatch): run only when *flag == 1
 template <int MODE>
-__device__ __forceinline__ void qb_wc_body(const double* A, const double* B, const double* C, const double* D,
-                                           const double* lo, const double* hi, double* x, long long N2,
-                                           double (*qf)[5][QWC_CAP], long long (*qi)[QWC_CAP]) {
+__global__ void __launch_bounds__(QWC_NW * 32) quartic_batch_wc_kernel(const double* A, const double* B,
+                                                                      const double* C, const double* D,
+                                                                      const double* lo, const double* hi,
+                                                                      double* x, long long N2,
+                                                                      const int* flag = nullptr) {
+    if (flag && *flag != 1) return;  // the per-lane kernel takes this batch
+    __shared__ double qf[QWC_NW][5][QWC_CAP];  // trigonometric queue: [warp][b c d lo hi][slot]
+    __shared__ long long qi[QWC_NW][QWC_CAP];  // [warp][slot] quartic index
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     int qn = 0;  // queued trigonometric quartics (warp-uniform)
@@ -580,18 +588,6 @@ __device__ __forceinline__ void qb_wc_body(const double* A, const double* B, con
     }
 }
 
-// flag (the sampled dispatch): run only when *flag == 1
-template <int MODE>
-__global__ void __launch_bounds__(256) quartic_batch_wc_kernel(const double* A, const double* B,
-                                                               const double* C, const double* D,
-                                                               const double* lo, const double* hi,
-                                                               double* x, long long N2,
-                                                               const int* flag = nullptr) {
-    if (flag && *flag != 1) return;  // the per-lane kernel takes this batch
-    __shared__ double qf[8][5][QWC_CAP];  // [warp][b c d lo hi][slot]
-    __shared__ long long qi[8][QWC_CAP];  // [warp][slot] quartic index
-    qb_wc_body<MODE>(A, B, C, D, lo, hi, x, N2, qf, qi);
-}
 
 // Dispatch between the two batch kernels from a strided sample of the batch: one CTA
 // classifies 4096 quartics (every (N/4096)-th) and sets flag = 1 when both branches are
@@ -2132,8 +2128,8 @@ admm_status quartic_minimize_batch(const double* A, const double* B, const doubl
         const char* wc = getenv("ADMM_QB_WC");
         if (wc && (wc[0] == '0' || wc[0] == '1')) {
             if (wc[0] == '1') {
-                if (box_mode == 1) quartic_batch_wc_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
-                else quartic_batch_wc_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+                if (box_mode == 1) quartic_batch_wc_kernel<1><<<grid, QWC_NW * 32, 0, st>>>(A, B, C, D, lo, hi, x, N2);
+                else quartic_batch_wc_kernel<0><<<grid, QWC_NW * 32, 0, st>>>(A, B, C, D, lo, hi, x, N2);
             } else if (box_mode == 1) {
                 quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
             } else {
@@ -2149,10 +2145,10 @@ admm_status quartic_minimize_batch(const double* A, const double* B, const doubl
             quartic_sample_kernel<<<1, 512, 0, st>>>(A, B, C, D, N, flag);
             if (box_mode == 1) {
                 quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
-                quartic_batch_wc_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+                quartic_batch_wc_kernel<1><<<grid, QWC_NW * 32, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
             } else {
                 quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
-                quartic_batch_wc_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
+                quartic_batch_wc_kernel<0><<<grid, QWC_NW * 32, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
             }
         }
     } else {
