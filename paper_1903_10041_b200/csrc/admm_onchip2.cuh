@@ -28,10 +28,13 @@
 //    finished every read of iteration t;
 //  * residual checks without a grid barrier or fence: each row publishes its six
 //    maxima (tile 0's row warp) and its x_1 (the consensus warp) as LL words, then
-//    bumps a relaxed arrival counter; the row warp of every CTA polls the counter
-//    (one lane), reads all rows' words (retrying the rare word whose epoch is not
-//    yet visible), reduces them in a fixed order and takes the identical
-//    termination / rho decision (same inputs, same order => same bits everywhere).
+//    bumps a relaxed arrival counter; tile 0's row warp of every row polls the
+//    counter (one lane), reads all rows' words (retrying the rare word whose epoch
+//    is not yet visible), reduces them in a fixed order, takes the termination /
+//    rho decision (same inputs, same order => same bits in every row) and forwards
+//    it to the row's other CTAs with st.async on a per-check-parity mbarrier;
+//  * the consensus warp sends its k = 0 partial right after the cell on non-check
+//    iterations (the row update waits on it), before the cell's bookkeeping.
 
 #pragma once
 #include <cooperative_groups.h>
