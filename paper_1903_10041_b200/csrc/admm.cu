@@ -1260,9 +1260,8 @@ admm_status launch_cluster(admm_ctx* ctx, cluster_fn fn, const PPlan& pl) {
 struct C2Plan {
     bool ok = false;
     int T = 0, NW = 0, TC0 = 0, TC = 0, G = 0;
+    int k = 0;  // cells per bulk thread (the most loaded tile)
     size_t smem = 0;
-    long long key_q = -1, key_n = -1;
-    int key_m = -1, key_mode = -1;
 };
 
 size_t oc2_smem(int m, long long TCM, int T, int nw) {
@@ -1352,6 +1351,7 @@ C2Plan plan_cluster2(admm_ctx* ctx, const void* fn) {
         pl.TC0 = (int)c.TC0;
         pl.TC = (int)c.TC;
         pl.G = (int)(q * c.T);
+        pl.k = (int)std::max((c.TC0 + 32LL * (c.NW - 1) - 1) / (32LL * (c.NW - 1)), (c.TC + 32LL * c.NW - 1) / (32LL * c.NW));
         pl.smem = smem;
         return pl;
     }
@@ -1415,13 +1415,21 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
         if (!(gm && gm[0] == '1')) {
             // default: the message-passing cluster engine (admm_onchip2.cuh);
             // ADMM_CLUSTER_V=1: the barrier-based one (admm_onchip.cuh)
+            // default: the message-passing engine when its plan gives every bulk thread one
+            // cell (PHEV q <= ~75, toy); with several cells per thread the barrier engine
+            // measured faster (PHEV q = 100: 5.95 vs 7.18 us per iteration, profiles/r02g) and
+            // is taken when it fits.  ADMM_CLUSTER_V=1 / 2 (or a forced shape) pick one.
             const char* cv = getenv("ADMM_CLUSTER_V");
-            if (cv && cv[0] == '1') {
-                cfn = pick_cluster(ctx->m, ctx->params.box_mode);
-                cpl = plan_cluster(ctx, cfn);
-            } else {
+            const bool force1 = cv && cv[0] == '1';
+            const bool force2 = (cv && cv[0] == '2') || getenv("ADMM_CLUSTER_T") || getenv("ADMM_CLUSTER_WARPS");
+            if (!force1) {
                 c2fn = cluster2_pick(ctx->m, ctx->params.box_mode);
                 c2pl = plan_cluster2(ctx, c2fn);
+            }
+            if (force1 || (!force2 && (!c2pl.ok || c2pl.k >= 2))) {
+                cfn = pick_cluster(ctx->m, ctx->params.box_mode);
+                cpl = plan_cluster(ctx, cfn);
+                if (cpl.ok) c2pl.ok = false;
             }
         }
         if (!cpl.ok && !c2pl.ok) {

@@ -59,11 +59,11 @@ def compare_states(P, So, Sg, tol=1e-9):
 # (ADMM_SWEEP_RL=1).  Read at solver creation.
 ENGINES = ["stream", "cluster", "grid"]
 ALT_ENGINES = ["stream_l1", "stream_l2", "stream_legacy", "stream_fx", "stream_u4", "stream_pf",
-               "stream_pf2", "stream_rl", "cluster_v1", "cluster_t3w2", "cluster_t1w14"]
-_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "cluster_v1": 2, "cluster_t3w2": 2, "cluster_t1w14": 2, "stream_l1": 1, "stream_l2": 1, "stream_legacy": 1, "stream_fx": 1,
+               "stream_pf2", "stream_rl", "cluster_v1", "cluster_v2", "cluster_t3w2", "cluster_t1w14"]
+_EXEC = {"stream": 1, "cluster": 2, "grid": 2, "cluster_v1": 2, "cluster_v2": 2, "cluster_t3w2": 2, "cluster_t1w14": 2, "stream_l1": 1, "stream_l2": 1, "stream_legacy": 1, "stream_fx": 1,
          "stream_pf": 1, "stream_pf2": 1, "stream_u4": 1, "stream_rl": 1, 0: 0}
 _LEG = {"ADMM_SWEEP2": "0"}
-_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "cluster_v1": {"ADMM_CLUSTER_V": "1"},
+_ENV = {"grid": {"ADMM_PERSIST_GRID": "1"}, "cluster_v1": {"ADMM_CLUSTER_V": "1"}, "cluster_v2": {"ADMM_CLUSTER_V": "2"},
         "cluster_t3w2": {"ADMM_CLUSTER_T": "3", "ADMM_CLUSTER_WARPS": "2"},
         "cluster_t1w14": {"ADMM_CLUSTER_T": "1", "ADMM_CLUSTER_WARPS": "14"}, "stream_l1": {"ADMM_S2_L": "1"}, "stream_l2": {"ADMM_S2_L": "2"},
         "stream_legacy": _LEG, "stream_fx": {"ADMM_SWEEP_FX": "1", **_LEG},
@@ -94,11 +94,12 @@ def gpu_run(P, params, iters, mode="iterate", r_bar=None, sigma_bar=None, max_it
     else:
         info = s.solve(r_bar, sigma_bar, max_iter)
     finite = bool(np.isfinite(P["lo"]).all() and np.isfinite(P["hi"]).all())  # fixed-point row sums
-    if engine in ("cluster", "cluster_v1") and (iters or mode != "iterate") and P["n"] * P["q"] <= 50000 and finite:
-        # the on-chip engine the variant names actually ran (not a fallback)
-        want = {"cluster_v1": "persist_cluster_kernel"}.get(engine, "persist_cluster2_kernel")
+    if engine in ("cluster", "cluster_v1", "cluster_v2") and (iters or mode != "iterate") and P["n"] * P["q"] <= 50000 and finite:
+        # an on-chip engine ran (not a fallback); forced variants: the one they name
         got = L._lib.ENGINE_NAMES.get(s.engine()[0])
-        assert got == want, (engine, got)
+        want = {"cluster_v1": ("persist_cluster_kernel",), "cluster_v2": ("persist_cluster2_kernel",)}.get(
+            engine, ("persist_cluster_kernel", "persist_cluster2_kernel"))
+        assert got in want, (engine, got)
     S = s.state()
     x, x1, sol = s.solution()
     hist = s.history()
