@@ -270,7 +270,8 @@ void admm_destroy(admm_ctx* ctx);
    (6a) (box_mode PROJECT = clamp of the global minimiser,
    EXACT = minimiser over [lo[e], hi[e]], reading G3).  A >= 0 (A = 0: the
    convex quadratic).  All arrays are DEVICE pointers of length N (caller
-   owned); lo/hi may be NULL (unbounded).  Asynchronous on cuda_stream: one CTA
+   owned); lo/hi may be NULL (unbounded).  Asynchronous on cuda_stream (a 4-byte
+   stream-ordered allocation per call from a library-owned memory pool): one CTA
    classifies a strided sample of 4096 quartics and picks, on the device, the
    one-quartic-per-lane kernel (one branch dominates) or the warp-compacted one
    (both common: trigonometric-branch quartics are queued per warp so each branch

@@ -18,7 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
-#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -594,8 +594,6 @@ __global__ void __launch_bounds__(QWC_NW * 32) quartic_batch_wc_kernel(const dou
 // common (trigonometric share in [1/64, 63/64]); the per-lane kernel runs when flag == 0
 // and the warp-compacted one when flag == 1 (the other returns at once), so the choice
 // needs no host round trip.
-__device__ int g_qb_flag[64];
-
 __global__ void __launch_bounds__(512) quartic_sample_kernel(const double* A, const double* B, const double* C,
                                                              const double* D, long long N, int* flag) {
     // 512 threads x 8 samples, every load issued before any arithmetic (one memory round trip)
@@ -2115,6 +2113,33 @@ void admm_destroy(admm_ctx* ctx) {
     delete ctx;
 }
 
+}  // extern "C"
+
+namespace {
+// per-device stream-ordered pool of the batch dispatch's decision words (release threshold
+// = max: freed blocks stay in the pool, so an allocation per call costs no driver call)
+cudaMemPool_t qb_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = p;
+    }
+    return pools[dev];
+}
+}  // namespace
+
+extern "C" {
+
 admm_status quartic_minimize_batch(const double* A, const double* B, const double* C,
                                    const double* D, const double* lo, const double* hi, double* x,
                                    int64_t N, int32_t box_mode, void* cuda_stream) {
@@ -2144,12 +2169,13 @@ admm_status quartic_minimize_batch(const double* A, const double* B, const doubl
                 quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2);
             }
         } else {
-            // the decision lives in one of 64 device words used round-robin (calls in flight
-            // on several streams at once each get their own word)
-            static std::atomic<unsigned> next_slot{0};
-            int* flags = nullptr;
-            if (cudaGetSymbolAddress((void**)&flags, g_qb_flag) != cudaSuccess) return ADMM_ERR_CUDA;
-            int* flag = flags + (next_slot.fetch_add(1) % 64);
+            // the decision word is a stream-ordered allocation private to this call, from a
+            // library-owned pool that never trims (cheap reuse; calls on concurrent streams
+            // cannot share a word)
+            cudaMemPool_t pool = qb_pool(dev);
+            if (!pool) return ADMM_ERR_CUDA;
+            int* flag = nullptr;
+            if (cudaMallocFromPoolAsync((void**)&flag, sizeof(int), pool, st) != cudaSuccess) return ADMM_ERR_CUDA;
             quartic_sample_kernel<<<1, 512, 0, st>>>(A, B, C, D, N, flag);
             if (box_mode == 1) {
                 quartic_batch_vec_kernel<1><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
@@ -2158,6 +2184,7 @@ admm_status quartic_minimize_batch(const double* A, const double* B, const doubl
                 quartic_batch_vec_kernel<0><<<grid, bs, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
                 quartic_batch_wc_kernel<0><<<grid, QWC_NW * 32, 0, st>>>(A, B, C, D, lo, hi, x, N2, flag);
             }
+            cudaFreeAsync(flag, st);
         }
     } else {
         const int grid = (int)std::min<long long>((N + bs - 1) / bs, (long long)sms * 8);
