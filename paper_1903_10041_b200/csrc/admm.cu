@@ -1371,8 +1371,11 @@ admm_status launch_cluster2(admm_ctx* ctx, const void* fn, const C2Plan& pl) {
     ca.pub = (unsigned long long*)(ctx->ws + ctx->L.pub2);
     ca.chkv = (unsigned long long*)(ctx->ws + ctx->L.chkv2);
     ca.chkx = (unsigned long long*)(ctx->ws + ctx->L.chkx2);
-    ca.cnt = (unsigned*)(ctx->ws + ctx->L.cnt2);
+    ca.cnt = (unsigned long long*)(ctx->ws + ctx->L.cnt2);
     ca.prm = ctx->dparams;
+    // epochs are 32-bit iteration / check counts of the call: at most 2^31 iterations per
+    // launch (run_loop relaunches)
+    if (ca.prm.iter_limit - ctx->iter_host > (1LL << 31)) ca.prm.iter_limit = ctx->iter_host + (1LL << 31);
     // the same expressions as check_decide (admm_kernels.cuh), evaluated once
     ca.thr_hi = ctx->params.hi_ratio * ctx->params.r_bar / ctx->params.sigma_bar;
     ca.thr_lo = ctx->params.lo_ratio * ctx->params.r_bar / ctx->params.sigma_bar;
@@ -1456,6 +1459,13 @@ admm_status run_loop(admm_ctx* ctx, long long iter_limit, int stop_on_conv) {
     if (c2pl.ok) {
         st = launch_cluster2(ctx, c2fn, c2pl);
         if (st != ADMM_OK) return st;
+        while (iter_limit - ctx->iter_host > (1LL << 31)) {  // more than one launch's epochs
+            st = read_ctrl(ctx);
+            if (st != ADMM_OK) return st;
+            if (ctx->h_ctrl->done || ctx->iter_host >= iter_limit) break;
+            st = launch_cluster2(ctx, c2fn, c2pl);
+            if (st != ADMM_OK) return st;
+        }
     } else if (cpl.ok) {
         st = launch_cluster(ctx, cfn, cpl);
         if (st != ADMM_OK) return st;

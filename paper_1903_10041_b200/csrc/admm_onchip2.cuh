@@ -56,7 +56,7 @@ struct C2Args {
     unsigned long long* pub;              // [4][M][q] LL pairs: x_1 - nu   (epoch = iteration in call + 1)
     unsigned long long* chkv;             // [4][q][6] LL pairs: row check maxima (epoch = check in call + 1)
     unsigned long long* chkx;             // [4][M][q] LL pairs: x_1 at checks
-    unsigned* cnt;                        // check arrivals in this call (2 q per check), relaxed
+    unsigned long long* cnt;              // check arrivals in this call (2 q per check), relaxed
     double thr_hi, thr_lo;                // hi_ratio r_bar / sigma_bar, lo_ratio r_bar / sigma_bar
     DParams prm;                          // the call's parameters (kernel-parameter space, not L1)
 };
@@ -149,12 +149,12 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned bar, unsigned parity)
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void gred_add_relaxed(unsigned* p, unsigned v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void gred_add_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64c(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 // bits of a non-negative double order like the double (NaN above +inf)
@@ -241,11 +241,11 @@ __device__ __noinline__ void oc2_check(const C2Args& p, double* hist, int hist_c
             ll_store(cbuf + 2 * ((size_t)j * OC2_CHKV + lane), nbits_inv(mine), cep);
         }
         __syncwarp();
-        if (lane == 0) gred_add_relaxed(p.cnt, 1u);
+        if (lane == 0) gred_add_relaxed(p.cnt, 1ull);
         CPHASE(0)
-        const unsigned target = 2u * (unsigned)qq * (nchk + 1);
+        const unsigned long long target = 2ull * (unsigned long long)qq * (nchk + 1ull);
         if (lane == 0)
-            while (ld_relaxed_u32(p.cnt) < target) __nanosleep(20);
+            while (ld_relaxed_u64c(p.cnt) < target) __nanosleep(20);
         __syncwarp();
         CPHASE(1)
         // rows j = lane + 32 b: six maxima, x_1, (6c) contribution (LL words, re-read until current)
@@ -720,7 +720,7 @@ __global__ void __launch_bounds__(OC2_MAX_W * 32) persist_cluster2_kernel(KArgs 
                     ll_store(p.chkx + 2 * ((size_t)(nchk & (OC2_BUFS - 1)) * M * qq + (size_t)lane * qq + j),
                              c_x0, nchk + 1);
                 __syncwarp();
-                if (lane == 0) gred_add_relaxed(p.cnt, 1u);
+                if (lane == 0) gred_add_relaxed(p.cnt, 1ull);
             }
             if (lane == 0) {
                 s_v[0] = cell_tail<M>(xo, xk0, yy, vv, 1.0, is_check, my_r1, my_s3);
