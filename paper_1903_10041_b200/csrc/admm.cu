@@ -863,8 +863,16 @@ bool tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, co
     auto fn = tmap_encoder();
     if (!fn) return false;
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    // L2 promotion (experiments: ADMM_TMA_PROMO = 0 none / 64 / 128 / 256 bytes)
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* e = getenv("ADMM_TMA_PROMO")) {
+        const int v = atoi(e);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+              : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     return fn(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
