@@ -150,6 +150,17 @@ __device__ __forceinline__ unsigned long long s2_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ unsigned long long s2_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// two consecutive doubles through the non-coherent path with an L2 cache policy
+__device__ __forceinline__ void s2_ld2_keep(const double* p, double* o, unsigned long long pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(o[0]), "=d"(o[1])
+                 : "l"(p), "l"(pol));
+}
 template <bool EF>
 __device__ __forceinline__ void s2_tmap3(unsigned dst, const CUtensorMap* m, int c0, int c1, unsigned bar) {
     if constexpr (EF) asm volatile(
@@ -367,9 +378,10 @@ __global__ void __launch_bounds__(S2_NT, L == 1 ? 3 : (M <= 2 ? SWEEP2_MINB : 2)
                         s2_ldL<double, L>(sp + C::BOFF + (size_t)i * TL * 8 + 8 * L * lane, lo);
                         s2_ldL<double, L>(sp + C::BOFF + (size_t)(M + i) * TL * 8 + 8 * L * lane, hi);
                     } else if constexpr (L == 2) {
-                        const double2 tl = __ldg(reinterpret_cast<const double2*>(a.lo + (long long)i * a.n_pad + k));
-                        const double2 th = __ldg(reinterpret_cast<const double2*>(a.hi + (long long)i * a.n_pad + k));
-                        lo[0] = tl.x; lo[1] = tl.y; hi[0] = th.x; hi[1] = th.y;
+                        // the box is re-read by every row: keep it in L2 (evict-last hint)
+                        const unsigned long long pol_keep = s2_evict_last();
+                        s2_ld2_keep(a.lo + (long long)i * a.n_pad + k, lo, pol_keep);
+                        s2_ld2_keep(a.hi + (long long)i * a.n_pad + k, hi, pol_keep);
                     } else {
                         lo[0] = __ldg(a.lo + (long long)i * a.n_pad + k);
                         hi[0] = __ldg(a.hi + (long long)i * a.n_pad + k);
