@@ -863,8 +863,11 @@ bool tmap(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, co
     auto fn = tmap_encoder();
     if (!fn) return false;
     const cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    // L2 promotion (experiments: ADMM_TMA_PROMO = 0 none / 64 / 128 / 256 bytes)
-    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    // L2 promotion 64 B: with 256 B a q = 1e5 sweep launch read 10.85 GB from DRAM against the
+    // 9.63 GB algorithmic (the promoted blocks straddle the 64-B-aligned row segments), with
+    // 64 B it reads 9.63 GB and is 1.8 % faster (profiles/r02i/promo_*); experiments:
+    // ADMM_TMA_PROMO = 0 none / 64 / 128 / 256 bytes
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     if (const char* e = getenv("ADMM_TMA_PROMO")) {
         const int v = atoi(e);
         promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
